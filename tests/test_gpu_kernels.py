@@ -1,0 +1,154 @@
+"""K1/K2 routing and K4 W4 GEMV on the B200 vs the CPU oracle."""
+
+import ctypes as Cc
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import routing_ref as RR
+from oracle import w4_ref as WR
+from paper_2509_07379_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+
+
+def _bf16_bits(t):
+    return t.view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def _rand_bf16(shape, std, gen):
+    return (torch.randn(shape, generator=gen) * std).to(torch.bfloat16)
+
+
+@pytest.mark.parametrize("T,d,M,k", [(1, 4096, 8, 2), (64, 256, 8, 2), (512, 4096, 8, 2), (37, 6144, 8, 2),
+                                     (5, 512, 16, 4)])
+def test_gate_topk_bit_exact(T, d, M, k, cuda):
+    g = torch.Generator().manual_seed(T * 7 + d)
+    x = _rand_bf16((T, d), 1.0, g)
+    wg = _rand_bf16((M, d), 0.02, g)
+    if T == 5:  # force exact ties: duplicate expert rows
+        wg[3] = wg[1]
+    xd, wd = x.to(cuda), wg.to(cuda)
+    idx = torch.empty((T, k), dtype=torch.int32, device=cuda)
+    w = torch.empty((T, k), dtype=torch.float32, device=cuda)
+    lg = torch.empty((T, M), dtype=torch.float64, device=cuda)
+    cnt = torch.zeros(M, dtype=torch.int32, device=cuda)
+    hist = torch.zeros((T, 3 * k), dtype=torch.int32, device=cuda)
+    _lib.call("ds_gate_topk", _lib.ptr(xd), _lib.ptr(wd), T, d, M, k, _lib.ptr(idx), _lib.ptr(w),
+              _lib.ptr(lg), _lib.ptr(cnt), _lib.ptr(hist), 3 * k, 1, _lib.stream_ptr())
+    torch.cuda.synchronize()
+    ref_lg = RR.gate_logits(_bf16_bits(x), _bf16_bits(wg))
+    assert np.array_equal(lg.cpu().numpy(), ref_lg)           # bitwise f64 logits
+    ref_idx, ref_w = RR.topk_route(ref_lg, k)
+    assert np.array_equal(idx.cpu().numpy(), ref_idx)
+    assert np.allclose(w.cpu().numpy(), ref_w, rtol=1e-6, atol=0)
+    assert np.array_equal(cnt.cpu().numpy(), np.bincount(ref_idx.reshape(-1), minlength=M))
+    h = hist.cpu().numpy()
+    assert np.array_equal(h[:, k:2 * k], ref_idx + 1) and not h[:, :k].any()
+
+
+@pytest.mark.parametrize("T,M,k", [(1, 8, 2), (512, 8, 2), (3000, 8, 2), (100, 16, 4)])
+def test_permute_and_combine(T, M, k, cuda):
+    rng = np.random.default_rng(T)
+    idx = np.sort(np.stack([rng.choice(M, k, replace=False) for _ in range(T)]), axis=1).astype(np.int32)
+    d = 256
+    x = _rand_bf16((T, d), 1.0, torch.Generator().manual_seed(1))
+    offs = torch.empty(M + 1, dtype=torch.int32, device=cuda)
+    pos = torch.empty(T * k, dtype=torch.int32, device=cuda)
+    src = torch.empty(T * k, dtype=torch.int32, device=cuda)
+    xp = torch.empty((T * k, d), dtype=torch.bfloat16, device=cuda)
+    idx_d = torch.from_numpy(idx).to(cuda)
+    xd = x.to(cuda)
+    _lib.call("ds_permute", _lib.ptr(idx_d), _lib.ptr(xd), T, d, M, k, _lib.ptr(offs), _lib.ptr(pos),
+              _lib.ptr(src), _lib.ptr(xp), _lib.stream_ptr())
+    torch.cuda.synchronize()
+    r_off, r_pos, r_src = RR.permute(idx, M)
+    assert np.array_equal(offs.cpu().numpy(), r_off)
+    assert np.array_equal(pos.cpu().numpy(), r_pos)
+    assert np.array_equal(src.cpu().numpy(), r_src)
+    assert torch.equal(xp.cpu(), x[torch.from_numpy(r_src).long()])
+    # combine
+    y = torch.randn((T * k, d), generator=torch.Generator().manual_seed(2))
+    wts = torch.rand((T, k), generator=torch.Generator().manual_seed(3))
+    out = torch.empty((T, d), dtype=torch.bfloat16, device=cuda)
+    yd, wd = y.to(cuda), wts.to(cuda)
+    _lib.call("ds_unpermute_combine", _lib.ptr(yd), _lib.ptr(pos), _lib.ptr(wd), _lib.ptr(xd), T, d, k,
+              _lib.ptr(out), _lib.stream_ptr())
+    torch.cuda.synchronize()
+    ref = RR.combine(y.numpy(), r_pos, wts.numpy(), x.float().numpy())
+    assert np.array_equal(out.float().cpu().numpy(), ref)
+
+
+def _layout(d, ff, G):
+    offs = (Cc.c_size_t * 9)()
+    total = _lib.query("ds_w4_expert_layout", d, ff, G, Cc.byref(offs))
+    return list(offs), total
+
+
+def _expert_struct(blob, offs):
+    base = blob.data_ptr()
+    e = _lib.W4Expert()
+    for m, lin in enumerate((e.w1, e.w3, e.w2)):
+        lin.codes, lin.scales, lin.zeros = base + offs[m], base + offs[3 + m], base + offs[6 + m]
+    return e
+
+
+@pytest.mark.parametrize("d,ff", [(256, 896), (4096, 14336)])
+def test_w4_generate_matches_oracle(d, ff, cuda):
+    G = 128
+    offs, total = _layout(d, ff, G)
+    blob = torch.empty(total, dtype=torch.uint8, device=cuda)
+    blob.zero_()
+    _lib.call("ds_w4_generate", 1234, 3, 5, d, ff, G, _lib.ptr(blob), _lib.stream_ptr())
+    torch.cuda.synchronize()
+    ref = WR.gen_expert_blob(1234, 3, 5, d, ff, G)
+    assert np.array_equal(blob.cpu().numpy(), ref)
+
+
+def test_w4_dequant_bit_exact(cuda):
+    d, ff, G = 256, 896, 128
+    offs, total = _layout(d, ff, G)
+    blob = torch.zeros(total, dtype=torch.uint8, device=cuda)
+    _lib.call("ds_w4_generate", 9, 0, 1, d, ff, G, _lib.ptr(blob), _lib.stream_ptr())
+    e = _expert_struct(blob, offs)
+    for m, (K, N, lin) in enumerate([(d, ff, e.w1), (d, ff, e.w3), (ff, d, e.w2)]):
+        out = torch.empty((N, K), dtype=torch.bfloat16, device=cuda)
+        _lib.call("ds_w4_dequant", Cc.byref(lin), K, N, G, _lib.ptr(out), _lib.stream_ptr())
+        torch.cuda.synchronize()
+        c, s, z = WR.gen_linear(9, 0, 1, m, K, N, G)
+        assert np.array_equal(_bf16_bits(out), WR.dequant(c, s, z, K, N, G))
+
+
+@pytest.mark.parametrize("d,ff,R", [(256, 896, 1), (4096, 14336, 1), (4096, 14336, 3), (6144, 16384, 1),
+                                    (256, 896, 6)])
+def test_w4_gemv_vs_fp32_reference(d, ff, R, cuda):
+    G = 128
+    offs, total = _layout(d, ff, G)
+    blob = torch.zeros(total, dtype=torch.uint8, device=cuda)
+    _lib.call("ds_w4_generate", 77, 2, 3, d, ff, G, _lib.ptr(blob), _lib.stream_ptr())
+    e = _expert_struct(blob, offs)
+    x = _rand_bf16((R, d), 1.0, torch.Generator().manual_seed(5))
+    xd = x.to(cuda)
+    h = torch.empty((R, ff), dtype=torch.bfloat16, device=cuda)
+    _lib.call("ds_w4_swiglu_gemv", _lib.ptr(xd), R, Cc.byref(e), d, ff, G, _lib.ptr(h), _lib.stream_ptr())
+    rw = torch.rand(R, generator=torch.Generator().manual_seed(6)).to(cuda)
+    acc = torch.zeros((R, d), dtype=torch.float32, device=cuda)
+    _lib.call("ds_w4_down_gemv", _lib.ptr(h), R, Cc.byref(e), d, ff, G, _lib.ptr(rw), 1, _lib.ptr(acc),
+              _lib.stream_ptr())
+    torch.cuda.synchronize()
+    # fp32 reference on the bit-exact dequantised weights (device dequant == oracle, tested above)
+    W = {}
+    for m, (K, N, lin) in enumerate([(d, ff, e.w1), (d, ff, e.w3), (ff, d, e.w2)]):
+        out = torch.empty((N, K), dtype=torch.bfloat16, device=cuda)
+        _lib.call("ds_w4_dequant", Cc.byref(lin), K, N, G, _lib.ptr(out), _lib.stream_ptr())
+        W[m] = out.double()
+    xf = xd.double()
+    a, b = xf @ W[0].T, xf @ W[1].T          # f64 reference (no TF32 anywhere)
+    h_ref = (torch.nn.functional.silu(a) * b)
+    hb = h.double()
+    rel = (hb - h_ref).norm() / h_ref.norm()
+    assert rel < 4e-3, rel                   # h is rounded to bf16 (2^-9 relative)
+    y_ref = (hb @ W[2].T) * rw.double()[:, None]
+    rel2 = (acc.double() - y_ref).norm() / y_ref.norm()
+    assert rel2 < 1e-5, rel2                 # f32 accumulation only
