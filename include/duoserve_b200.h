@@ -168,13 +168,19 @@ int ds_w4_down_gemv(const void *h, int R, const ds_w4_expert *e, int d, int ff, 
                     const float *route_w, int route_stride, float *acc, void *stream);
 /* out[r] = bf16(resid[r] + acc[r]) and acc zeroed for the next layer.      */
 int ds_combine_finalize(float *acc, const void *resid, int R, int d, void *out, void *stream);
-/* Prefill grouped FFN (K3): for experts e in [0,E): rows
+/* Prefill grouped FFN (K3): for experts e in [0,E) (E <= 16): rows
  * [offsets[e], offsets[e+1]) of xperm [*, d] bf16 through experts[e];
- * y f32 [*, d] (un-weighted expert outputs).  h is bf16 [*, ff] scratch.
- * tcgen05.mma (kind::f16, f32 accumulators in TMEM), weights dequantised
- * into UMMA SWIZZLE_128B shared-memory tiles.                              */
+ * y f32 [offsets[E], d] (un-weighted expert outputs).  h is bf16
+ * [offsets[E], ff] scratch.  offsets and experts are HOST arrays (the host
+ * scheduler knows the grouping; weights are device pointers, e.g. cache
+ * slots).  tcgen05.mma (kind::f16, f32 accumulators in TMEM, BM=128 weight
+ * rows x BN=128 token rows), activation tiles by TMA (SWIZZLE_128B), W4
+ * dequantised into UMMA SWIZZLE_128B shared-memory tiles.  Split-K partials
+ * of the down projection are reduced in a fixed order (deterministic).     */
+size_t ds_w4_grouped_ffn_workspace(int total_rows, int d, int ff);
 int ds_w4_grouped_ffn(const void *xperm, const int32_t *offsets, int E, const ds_w4_expert *experts,
-                      int d, int ff, int G, void *h, float *y, void *stream);
+                      int d, int ff, int G, void *h, float *y, void *workspace,
+                      size_t workspace_bytes, void *stream);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -79,6 +79,8 @@ _SIGS = {
     "ds_w4_swiglu_gemv": (_I, [_P, _I, C.POINTER(W4Expert), _I, _I, _I, _P, _P]),
     "ds_w4_down_gemv": (_I, [_P, _I, C.POINTER(W4Expert), _I, _I, _I, _P, _I, _P, _P]),
     "ds_combine_finalize": (_I, [_P, _P, _I, _I, _P, _P]),
+    "ds_w4_grouped_ffn_workspace": (_SZ, [_I, _I, _I]),
+    "ds_w4_grouped_ffn": (_I, [_P, C.POINTER(_I), _I, C.POINTER(W4Expert), _I, _I, _I, _P, _P, _P, _SZ, _P]),
 }
 
 _lib = None

@@ -1,0 +1,408 @@
+// K3 — prefill grouped W4 SwiGLU expert FFN on the 5th-gen tensor cores.
+//
+// Per expert e with rows [row_start, row_start + rows) of the grouped
+// activations (K2 permute output):
+//   GEMM1  H[m, n]  = bf16( silu(X W1)[m, n] * (X W3)[m, n] )     n < ff
+//   GEMM2  Y[m, n'] = (H W2)[m, n']  (f32, split-K partials reduced in a
+//                                      fixed order -> deterministic)
+// Swap-AB: the weight output dimension is the UMMA M side (128 rows per
+// CTA tile), the expert's token rows are the UMMA N side (BN = 128), so
+// small per-expert row counts still fill M=128 tiles.
+//
+// Per CTA (one 128 x BN output tile, one expert):
+//   warp 0      TMA producer: activation tile [BN x 64] bf16, SWIZZLE_128B
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//               (kind::f16, f32 accumulators in TMEM: NMAT x BN columns)
+//   warps 2-9   W4 dequant producers: 16-byte streaming loads of packed int4
+//               codes, w = bf16((q - z) * s) via the bf16 exponent trick +
+//               HSUB2/HMUL2 (bit-identical to ds_w4_dequant), written into
+//               the UMMA K-major SWIZZLE_128B layout, fence.proxy.async, arrive
+//   warps 2-5   epilogue: tcgen05.ld TMEM -> registers -> SwiGLU -> global
+// Stages are tied by mbarriers: full_b (TMA tx bytes), full_a (256 dequant
+// arrivals), empty (tcgen05.commit), tmem_full (final commit).
+#include "ds_common.cuh"
+#include "sm100.cuh"
+
+#include <cuda.h>
+
+namespace ds {
+namespace {
+
+using namespace sm100;
+
+constexpr int BM = 128;         // weight rows per tile (UMMA M)
+constexpr int BN = 128;         // activation rows per tile (UMMA N)
+constexpr int BK = 64;          // K per stage (one 128-byte swizzle atom of bf16)
+constexpr int UK = 16;          // K per tcgen05.mma (kind::f16)
+constexpr int kMaxExperts = 16;
+constexpr int kThreads = 320;   // 10 warps
+constexpr int kDequantThreads = 256;
+constexpr int kTileBytes = 128 * 128;  // 128 rows x 128 B
+
+struct W4Mat {
+    const uint32_t* codes;
+    const uint16_t* scales;
+    const uint8_t* zeros;
+};
+
+struct GemmArgs {
+    int K, N, G;
+    int kt_per_split;   // k-tiles (of BK) per split
+    int splits;
+    int total_rows;
+    int row_start[kMaxExperts];
+    int rows[kMaxExperts];
+    W4Mat w[kMaxExperts][2];
+    void* out;          // NMAT=2: bf16 H [total_rows, N]; NMAT=1: f32 [splits][total_rows][N]
+};
+
+template <int NMAT>
+struct Smem {
+    static constexpr int STAGES = NMAT == 2 ? 3 : 4;
+    static constexpr int A_BYTES = NMAT * kTileBytes;
+    static constexpr int B_BYTES = BN * 128;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+    static constexpr int TOTAL = BAR_OFF + 256 + 1024;  // + barriers + alignment slack
+};
+
+__device__ __forceinline__ uint32_t bf16x2_bits(__nv_bfloat162 v) {
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ __nv_bfloat162 as_bf162(uint32_t v) {
+    return *reinterpret_cast<__nv_bfloat162*>(&v);
+}
+
+// 32 codes (one uint4) -> 4 swizzled 16-byte chunks of bf16 weights
+__device__ __forceinline__ void dequant32(const uint4 c, uint32_t zz, uint32_t ss, uint8_t* row_base,
+                                          int chunk0, int swz) {
+    const uint32_t cw[4] = {c.x, c.y, c.z, c.w};
+    const __nv_bfloat162 z2 = as_bf162(zz), s2 = as_bf162(ss);
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+        uint32_t o[4];
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            const __nv_bfloat162 v = as_bf162(nib_pair_magic(cw[w] >> (4 * p)));
+            o[p] = bf16x2_bits(__hmul2(__hsub2(v, z2), s2));   // exact (q-z), one rounding
+        }
+        uint4* dst = reinterpret_cast<uint4*>(row_base + (((chunk0 + w) ^ swz) << 4));
+        *dst = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+}
+
+template <int NMAT>
+__global__ void __launch_bounds__(kThreads, 1)
+w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constant__ GemmArgs args) {
+    using S = Smem<NMAT>;
+    constexpr int STAGES = S::STAGES;
+    constexpr uint32_t TMEM_COLS = NMAT * BN;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full_b = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
+    uint64_t* full_a = full_b + STAGES;
+    uint64_t* empty = full_a + STAGES;
+    uint64_t* tmem_full = empty + STAGES;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+    const int e = blockIdx.z;
+    const int rows = args.rows[e];
+    const int m0 = blockIdx.y * BN;
+    if (m0 >= rows) return;                       // whole CTA exits before any barrier
+    const int n_blocks = args.N / BM;
+    const int nb = blockIdx.x % n_blocks;
+    const int split = blockIdx.x / n_blocks;
+    const int n0 = nb * BM;
+    const int kt0 = split * args.kt_per_split;
+    const int KT = args.kt_per_split;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full_b[s], 1);
+            mbar_init(&full_a[s], kDequantThreads);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(tmem_full, 1);
+        fence_mbar_init();
+        tma_prefetch_desc(&act_map);
+    }
+    if (warp == 1) tmem_alloc<TMEM_COLS>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------------------------------------------- TMA producer
+        if (lane == 0) {
+            const int row_coord = args.row_start[e] + m0;
+            for (int kt = 0; kt < KT; ++kt) {
+                const int s = kt % STAGES;
+                if (kt >= STAGES) mbar_wait(&empty[s], ((kt / STAGES) - 1) & 1);
+                uint8_t* b_tile = smem + s * S::STAGE_BYTES + S::A_BYTES;
+                mbar_expect_tx(&full_b[s], S::B_BYTES);
+                tma_load_2d(b_tile, &act_map, &full_b[s], (kt0 + kt) * BK, row_coord);
+            }
+        }
+    } else if (warp == 1) {
+        // -------------------------------------------------------- MMA issuer
+        if (lane == 0) {
+            const uint32_t idesc = idesc_bf16_f32(BM, BN);
+            for (int kt = 0; kt < KT; ++kt) {
+                const int s = kt % STAGES;
+                const uint32_t ph = (kt / STAGES) & 1;
+                mbar_wait(&full_b[s], ph);
+                mbar_wait(&full_a[s], ph);
+                tc_fence_after();
+                const uint32_t a_addr = smem_u32(smem + s * S::STAGE_BYTES);
+                const uint32_t b_addr = a_addr + S::A_BYTES;
+                const uint64_t bdesc = umma_desc_sw128(b_addr);
+#pragma unroll
+                for (int kk = 0; kk < BK / UK; ++kk) {
+#pragma unroll
+                    for (int j = 0; j < NMAT; ++j) {
+                        const uint64_t adesc = umma_desc_sw128(a_addr + j * kTileBytes);
+                        // advance along K inside the swizzle atom: +32 B = +2 (16-B units)
+                        mma_bf16(tmem_base + j * BN, adesc + 2 * kk, bdesc + 2 * kk, idesc,
+                                 (kt | kk) != 0);
+                    }
+                }
+                mma_commit(&empty[s]);
+            }
+            mma_commit(tmem_full);
+        }
+    } else {
+        // ------------------------------------------------ dequant producers
+        const int t = threadIdx.x - 64;          // 0..255
+        const int nl = t & 127, half = t >> 7;
+        const int n = n0 + nl;
+        const int K = args.K, G = args.G;
+        const int gpr = K / G;
+        const size_t row_words = (size_t)K / 8;
+        const W4Mat* W = args.w[e];
+        const int swz = nl & 7;
+        uint4 cur[NMAT];
+        uint16_t sc[NMAT];
+        uint8_t zb[NMAT];
+        auto load = [&](int kt, uint4 (&c)[NMAT], uint16_t (&s)[NMAT], uint8_t (&z)[NMAT]) {
+            const int kb = (kt0 + kt) * BK + 32 * half;
+            const size_t gi = (size_t)n * gpr + kb / G;
+#pragma unroll
+            for (int j = 0; j < NMAT; ++j) {
+                c[j] = ldg_nc_v4(W[j].codes + (size_t)n * row_words + kb / 8);
+                s[j] = __ldg(W[j].scales + gi);
+                z[j] = __ldg(W[j].zeros + (gi >> 1));
+            }
+        };
+        const size_t gi0 = 0;
+        (void)gi0;
+        uint4 nxt[NMAT];
+        uint16_t nsc[NMAT];
+        uint8_t nzb[NMAT];
+        load(0, cur, sc, zb);
+        if (KT > 1) load(1, nxt, nsc, nzb);
+        for (int kt = 0; kt < KT; ++kt) {
+            const int s = kt % STAGES;
+            if (kt >= STAGES) mbar_wait(&empty[s], ((kt / STAGES) - 1) & 1);
+            const int kb = (kt0 + kt) * BK + 32 * half;
+            const size_t gi = (size_t)n * gpr + kb / G;
+            uint8_t* a_tile = smem + s * S::STAGE_BYTES;
+#pragma unroll
+            for (int j = 0; j < NMAT; ++j) {
+                const uint32_t z = (zb[j] >> ((gi & 1) * 4)) & 15;
+                const uint32_t zz = (0x4300u | z) * 0x00010001u;
+                const uint32_t ss = (uint32_t)sc[j] * 0x00010001u;
+                dequant32(cur[j], zz, ss, a_tile + j * kTileBytes + nl * 128, 4 * half, swz);
+            }
+            fence_proxy_async_smem();
+            mbar_arrive(&full_a[s]);
+#pragma unroll
+            for (int j = 0; j < NMAT; ++j) {
+                cur[j] = nxt[j];
+                sc[j] = nsc[j];
+                zb[j] = nzb[j];
+            }
+            if (kt + 2 < KT) load(kt + 2, nxt, nsc, nzb);
+        }
+
+        // ---------------------------------------------------------- epilogue
+        if (warp < 6) {
+            const int q = warp & 3;                   // TMEM lane quadrant of this warp
+            const int nrow = n0 + 32 * q + lane;
+            mbar_wait(tmem_full, 0);
+            tc_fence_after();
+            const uint32_t lane_addr = tmem_base + ((uint32_t)(32 * q) << 16);
+            const int row0 = args.row_start[e] + m0;
+            const int valid = min(BN, rows - m0);
+            for (int c0 = 0; c0 < BN; c0 += 16) {
+                uint32_t d1[16];
+                tmem_ld16(lane_addr + c0, d1);
+                if constexpr (NMAT == 2) {
+                    uint32_t d3[16];
+                    tmem_ld16(lane_addr + BN + c0, d3);
+                    tmem_ld_wait();
+                    __nv_bfloat16* H = static_cast<__nv_bfloat16*>(args.out);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        if (c0 + i < valid) {
+                            const float a = __uint_as_float(d1[i]), b = __uint_as_float(d3[i]);
+                            const float sl = a / (1.0f + expf(-a));
+                            H[(size_t)(row0 + c0 + i) * args.N + nrow] = __float2bfloat16_rn(sl * b);
+                        }
+                    }
+                } else {
+                    tmem_ld_wait();
+                    float* Y = static_cast<float*>(args.out) + (size_t)split * args.total_rows * args.N;
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        if (c0 + i < valid) Y[(size_t)(row0 + c0 + i) * args.N + nrow] = __uint_as_float(d1[i]);
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<TMEM_COLS>(tmem_base);
+    }
+}
+
+__global__ void split_reduce_kernel(const float* __restrict__ part, int splits, size_t n,
+                                    float* __restrict__ y) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x) {
+        float acc = part[i];
+        for (int s = 1; s < splits; ++s) acc = __fadd_rn(acc, part[(size_t)s * n + i]);
+        y[i] = acc;
+    }
+}
+
+// ------------------------------------------------------------------ host
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                  CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                  CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+int make_act_map(CUtensorMap* map, const void* base, int rows, int K) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return fail(DS_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)K * 2};
+    cuuint32_t box[2] = {BK, BN};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(DS_ERR_ARG, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return DS_OK;
+}
+
+int choose_splits(int d, int mblocks_total) {
+    const int tiles = (d / BM) * (mblocks_total > 0 ? mblocks_total : 1);
+    int s = 1;
+    while (s < 8 && tiles * s * 2 <= num_sms()) s *= 2;
+    return s;
+}
+
+template <int NMAT>
+int launch_gemm(const CUtensorMap& map, const GemmArgs& a, int E, int max_mblocks, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(w4_gemm_kernel<NMAT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             Smem<NMAT>::TOTAL);
+        if (e != cudaSuccess) return cuda_status(e, "w4_gemm: smem attribute");
+        attr = true;
+    }
+    dim3 grid((a.N / BM) * a.splits, max_mblocks, E);
+    w4_gemm_kernel<NMAT><<<grid, kThreads, Smem<NMAT>::TOTAL, st>>>(map, a);
+    DS_LAUNCH_CHECK("w4_gemm launch");
+    return DS_OK;
+}
+
+}  // namespace
+}  // namespace ds
+
+using namespace ds;
+
+extern "C" size_t ds_w4_grouped_ffn_workspace(int total_rows, int d, int ff) {
+    (void)ff;
+    const int mb = (total_rows + BN - 1) / BN;
+    return (size_t)choose_splits(d, mb) * total_rows * d * sizeof(float);
+}
+
+extern "C" int ds_w4_grouped_ffn(const void* xperm, const int32_t* offsets, int E,
+                                 const ds_w4_expert* experts, int d, int ff, int G, void* h, float* y,
+                                 void* workspace, size_t workspace_bytes, void* stream) {
+    DS_CHECK_ARG(E >= 1 && E <= kMaxExperts, "ds_w4_grouped_ffn: 1 <= E <= %d", kMaxExperts);
+    DS_CHECK_ARG(d % BM == 0 && ff % BM == 0 && d % BK == 0 && ff % BK == 0,
+                 "ds_w4_grouped_ffn: d, ff must be multiples of 128");
+    DS_CHECK_ARG(G == 64 || G == 128, "ds_w4_grouped_ffn: G must be 64 or 128");
+    DS_CHECK_ARG(xperm && offsets && experts && h && y, "ds_w4_grouped_ffn: NULL pointer");
+    const int total_rows = offsets[E];
+    GemmArgs a1{}, a2{};
+    int max_mb = 0, mb_total = 0;
+    for (int i = 0; i < E; ++i) {
+        const int r = offsets[i + 1] - offsets[i];
+        DS_CHECK_ARG(r >= 0 && offsets[i] >= 0, "ds_w4_grouped_ffn: offsets must be non-decreasing");
+        a1.row_start[i] = a2.row_start[i] = offsets[i];
+        a1.rows[i] = a2.rows[i] = r;
+        const int mb = (r + BN - 1) / BN;
+        max_mb = mb > max_mb ? mb : max_mb;
+        mb_total += mb;
+        const ds_w4_linear* L[3] = {&experts[i].w1, &experts[i].w3, &experts[i].w2};
+        for (int j = 0; j < 3; ++j)
+            DS_CHECK_ARG(L[j]->codes && L[j]->scales && L[j]->zeros, "ds_w4_grouped_ffn: NULL weights");
+        a1.w[i][0] = W4Mat{L[0]->codes, (const uint16_t*)L[0]->scales, L[0]->zeros};
+        a1.w[i][1] = W4Mat{L[1]->codes, (const uint16_t*)L[1]->scales, L[1]->zeros};
+        a2.w[i][0] = W4Mat{L[2]->codes, (const uint16_t*)L[2]->scales, L[2]->zeros};
+    }
+    if (total_rows == 0 || max_mb == 0) return DS_OK;
+    cudaStream_t st = as_stream(stream);
+    // GEMM1: K = d, N = ff
+    CUtensorMap map1, map2;
+    int rc = make_act_map(&map1, xperm, total_rows, d);
+    if (rc) return rc;
+    a1.K = d; a1.N = ff; a1.G = G; a1.kt_per_split = d / BK; a1.splits = 1;
+    a1.total_rows = total_rows; a1.out = h;
+    rc = launch_gemm<2>(map1, a1, E, max_mb, st);
+    if (rc) return rc;
+    // GEMM2: K = ff, N = d, split-K with a deterministic reduction
+    rc = make_act_map(&map2, h, total_rows, ff);
+    if (rc) return rc;
+    int splits = choose_splits(d, mb_total);
+    while (splits > 1 && (ff / BK) % splits) splits >>= 1;
+    const size_t need = (size_t)splits * total_rows * d * sizeof(float);
+    a2.K = ff; a2.N = d; a2.G = G; a2.kt_per_split = (ff / BK) / splits; a2.splits = splits;
+    a2.total_rows = total_rows;
+    if (splits == 1) {
+        a2.out = y;
+    } else {
+        if (!workspace || workspace_bytes < need)
+            return fail(DS_ERR_WORKSPACE, "ds_w4_grouped_ffn: workspace %zu < %zu", workspace_bytes, need);
+        a2.out = workspace;
+    }
+    rc = launch_gemm<1>(map2, a2, E, max_mb, st);
+    if (rc) return rc;
+    if (splits > 1) {
+        const size_t n = (size_t)total_rows * d;
+        int grid = (int)((n + 255) / 256);
+        if (grid > 4 * num_sms()) grid = 4 * num_sms();
+        split_reduce_kernel<<<grid, 256, 0, st>>>(static_cast<const float*>(workspace), splits, n, y);
+        DS_LAUNCH_CHECK("ds_w4_grouped_ffn: split reduce");
+    }
+    return DS_OK;
+}
