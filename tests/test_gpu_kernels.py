@@ -152,3 +152,49 @@ def test_w4_gemv_vs_fp32_reference(d, ff, R, cuda):
     y_ref = (hb @ W[2].T) * rw.double()[:, None]
     rel2 = (acc.double() - y_ref).norm() / y_ref.norm()
     assert rel2 < 1e-5, rel2                 # f32 accumulation only
+
+
+def _dense(e, d, ff, G, cuda):
+    W = []
+    for K, N, lin in [(d, ff, e.w1), (d, ff, e.w3), (ff, d, e.w2)]:
+        out = torch.empty((N, K), dtype=torch.bfloat16, device=cuda)
+        _lib.call("ds_w4_dequant", Cc.byref(lin), K, N, G, _lib.ptr(out), _lib.stream_ptr())
+        W.append(out.double())
+    return W
+
+
+@pytest.mark.parametrize("d,ff,rows", [(256, 896, [7, 64, 0, 130]), (4096, 14336, [128, 100, 3]),
+                                       (6144, 16384, [200]), (256, 896, [1])])
+def test_w4_grouped_ffn_tcgen05(d, ff, rows, cuda):
+    """K3 (tcgen05/TMEM/TMA) vs an f64 reference on the bit-exact dequantised weights."""
+    G = 128
+    offs, total = _layout(d, ff, G)
+    E = len(rows)
+    blobs = [torch.zeros(total, dtype=torch.uint8, device=cuda) for _ in range(E)]
+    for i, b in enumerate(blobs):
+        _lib.call("ds_w4_generate", 5, 1, i, d, ff, G, _lib.ptr(b), _lib.stream_ptr())
+    experts = (_lib.W4Expert * E)(*[_expert_struct(b, offs) for b in blobs])
+    offsets = np.concatenate([[0], np.cumsum(rows)]).astype(np.int32)
+    R = int(offsets[-1])
+    x = _rand_bf16((max(R, 1), d), 1.0, torch.Generator().manual_seed(11)).to(cuda)
+    h = torch.empty((max(R, 1), ff), dtype=torch.bfloat16, device=cuda)
+    y = torch.empty((max(R, 1), d), dtype=torch.float32, device=cuda)
+    ws_bytes = _lib.query("ds_w4_grouped_ffn_workspace", R, d, ff)
+    ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=cuda)
+    off_c = (Cc.c_int * (E + 1))(*offsets.tolist())
+    _lib.call("ds_w4_grouped_ffn", _lib.ptr(x), off_c, E, experts, d, ff, G, _lib.ptr(h), _lib.ptr(y),
+              _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
+    torch.cuda.synchronize()
+    for i in range(E):
+        lo, hi = int(offsets[i]), int(offsets[i + 1])
+        if lo == hi:
+            continue
+        W1, W3, W2 = _dense(experts[i], d, ff, G, cuda)
+        xf = x[lo:hi].double()
+        h_ref = torch.nn.functional.silu(xf @ W1.T) * (xf @ W3.T)
+        hb = h[lo:hi].double()
+        rel = ((hb - h_ref).norm() / h_ref.norm()).item()
+        assert rel < 4e-3, (i, rel)
+        y_ref = hb @ W2.T
+        rel2 = ((y[lo:hi].double() - y_ref).norm() / y_ref.norm()).item()
+        assert rel2 < 1e-5, (i, rel2)
