@@ -141,3 +141,14 @@ def expert_dense(seed, layer, expert, d, ff, G):
         c, s, z = gen_linear(seed, layer, expert, m, K, N, G)
         out.append(bf16_bits_to_f32(dequant(c, s, z, K, N, G)).T.copy())
     return out
+
+
+def dequant_exact(codes, scales, zeros, K, N, G) -> np.ndarray:
+    """float64 [N, K] of (q - z) * s WITHOUT the bf16 rounding: the decode
+    GEMV (K4) factorises the group scale out of the dot product,
+        sum_k x_k (q_k - z) s = s * (sum_k x_k (128+q_k) - (128+z) sum_k x_k),
+    so its reference weights are the exact products."""
+    q = unpack_codes(codes).astype(np.float64)
+    z = np.repeat(unpack_zeros(zeros, N, K // G).astype(np.float64), G, axis=1)
+    s = np.repeat(bf16_bits_to_f32(scales).astype(np.float64), G, axis=1)
+    return (q - z) * s

@@ -1,0 +1,88 @@
+"""torch-facing wrappers of the C-ABI hot-path kernels (device tensors in,
+device tensors out, launched on the current stream).  No CPU fallback."""
+
+from __future__ import annotations
+
+import ctypes as C
+from functools import lru_cache
+
+import torch
+
+from . import _lib
+from ._lib import ptr, stream_ptr
+
+
+@lru_cache(maxsize=None)
+def expert_layout(d: int, ff: int, G: int):
+    """(section offsets [9], total bytes) of one W4 expert blob."""
+    offs = (C.c_size_t * 9)()
+    total = _lib.query("ds_w4_expert_layout", d, ff, G, C.byref(offs))
+    if total == 0:
+        raise ValueError(f"unsupported expert shape d={d} ff={ff} G={G}")
+    return tuple(offs), int(total)
+
+
+def expert_struct(base_ptr: int, d: int, ff: int, G: int) -> _lib.W4Expert:
+    offs, _ = expert_layout(d, ff, G)
+    e = _lib.W4Expert()
+    for m, lin in enumerate((e.w1, e.w3, e.w2)):
+        lin.codes, lin.scales, lin.zeros = base_ptr + offs[m], base_ptr + offs[3 + m], base_ptr + offs[6 + m]
+    return e
+
+
+def w4_generate(seed: int, layer: int, expert: int, d: int, ff: int, G: int, blob: torch.Tensor) -> None:
+    _lib.call("ds_w4_generate", seed, layer, expert, d, ff, G, ptr(blob), stream_ptr())
+
+
+def gate_topk(x: torch.Tensor, wg: torch.Tensor, k: int, idx: torch.Tensor, w: torch.Tensor,
+              counts: torch.Tensor | None = None, hist: torch.Tensor | None = None, layer: int = 0,
+              logits: torch.Tensor | None = None) -> None:
+    T, d = x.shape
+    M = wg.shape[0]
+    stride = hist.shape[-1] if hist is not None else 0
+    _lib.call("ds_gate_topk", ptr(x), ptr(wg), T, d, M, k, ptr(idx), ptr(w), ptr(logits), ptr(counts),
+              ptr(hist), stride, layer, stream_ptr())
+
+
+def permute(idx: torch.Tensor, x: torch.Tensor, M: int, offsets, pos, src, xperm) -> None:
+    T, k = idx.shape
+    _lib.call("ds_permute", ptr(idx), ptr(x), T, x.shape[1], M, k, ptr(offsets), ptr(pos), ptr(src),
+              ptr(xperm), stream_ptr())
+
+
+def unpermute_combine(y: torch.Tensor, pos, w, resid, out) -> None:
+    T, k = w.shape
+    _lib.call("ds_unpermute_combine", ptr(y), ptr(pos), ptr(w), ptr(resid), T, resid.shape[1], k, ptr(out),
+              stream_ptr())
+
+
+def swiglu_gemv(x: torch.Tensor, e: _lib.W4Expert, d: int, ff: int, G: int, h: torch.Tensor) -> None:
+    _lib.call("ds_w4_swiglu_gemv", ptr(x), x.shape[0], C.byref(e), d, ff, G, ptr(h), stream_ptr())
+
+
+def down_gemv(h: torch.Tensor, e: _lib.W4Expert, d: int, ff: int, G: int, route_w: torch.Tensor,
+              route_stride: int, acc: torch.Tensor) -> None:
+    _lib.call("ds_w4_down_gemv", ptr(h), h.shape[0], C.byref(e), d, ff, G, ptr(route_w), route_stride, ptr(acc),
+              stream_ptr())
+
+
+def combine_finalize(acc: torch.Tensor, resid: torch.Tensor, out: torch.Tensor) -> None:
+    _lib.call("ds_combine_finalize", ptr(acc), ptr(resid), resid.shape[0], resid.shape[1], ptr(out), stream_ptr())
+
+
+def grouped_ffn_workspace(rows: int, d: int, ff: int) -> int:
+    return int(_lib.query("ds_w4_grouped_ffn_workspace", rows, d, ff))
+
+
+def grouped_ffn(xperm: torch.Tensor, offsets: list, experts: list, d: int, ff: int, G: int, h: torch.Tensor,
+                y: torch.Tensor, ws: torch.Tensor) -> None:
+    E = len(experts)
+    off = (C.c_int * (E + 1))(*[int(o) for o in offsets])
+    arr = (_lib.W4Expert * E)(*experts)
+    _lib.call("ds_w4_grouped_ffn", ptr(xperm), off, E, arr, d, ff, G, ptr(h), ptr(y), ptr(ws), ws.numel(),
+              stream_ptr())
+
+
+def route_histogram(paths: torch.Tensor, M: int, pop_counts: torch.Tensor, aff_counts: torch.Tensor) -> None:
+    N, L, k = paths.shape
+    _lib.call("ds_route_histogram", ptr(paths), N, L, M, k, ptr(pop_counts), ptr(aff_counts), stream_ptr())

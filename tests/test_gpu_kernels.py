@@ -122,7 +122,10 @@ def test_w4_dequant_bit_exact(cuda):
 
 @pytest.mark.parametrize("d,ff,R", [(256, 896, 1), (4096, 14336, 1), (4096, 14336, 3), (6144, 16384, 1),
                                     (256, 896, 6)])
-def test_w4_gemv_vs_fp32_reference(d, ff, R, cuda):
+def test_w4_gemv_vs_f64_reference(d, ff, R, cuda):
+    """K4 decode GEMV.  It factorises the group scale out of the dot product,
+    so its reference weights are the EXACT (q - z) * s (oracle.w4_ref.dequant_exact);
+    against those the only error is f32 accumulation."""
     G = 128
     offs, total = _layout(d, ff, G)
     blob = torch.zeros(total, dtype=torch.uint8, device=cuda)
@@ -137,22 +140,17 @@ def test_w4_gemv_vs_fp32_reference(d, ff, R, cuda):
     _lib.call("ds_w4_down_gemv", _lib.ptr(h), R, Cc.byref(e), d, ff, G, _lib.ptr(rw), 1, _lib.ptr(acc),
               _lib.stream_ptr())
     torch.cuda.synchronize()
-    # fp32 reference on the bit-exact dequantised weights (device dequant == oracle, tested above)
-    W = {}
-    for m, (K, N, lin) in enumerate([(d, ff, e.w1), (d, ff, e.w3), (ff, d, e.w2)]):
-        out = torch.empty((N, K), dtype=torch.bfloat16, device=cuda)
-        _lib.call("ds_w4_dequant", Cc.byref(lin), K, N, G, _lib.ptr(out), _lib.stream_ptr())
-        W[m] = out.double()
+    W = [torch.from_numpy(WR.dequant_exact(*WR.gen_linear(77, 2, 3, m, K, N, G), K, N, G)).to(cuda)
+         for m, (K, N) in enumerate([(d, ff), (d, ff), (ff, d)])]
     xf = xd.double()
-    a, b = xf @ W[0].T, xf @ W[1].T          # f64 reference (no TF32 anywhere)
-    h_ref = (torch.nn.functional.silu(a) * b)
+    a, b = xf @ W[0].T, xf @ W[1].T
+    h_ref = torch.nn.functional.silu(a) * b
     hb = h.double()
-    rel = (hb - h_ref).norm() / h_ref.norm()
-    assert rel < 4e-3, rel                   # h is rounded to bf16 (2^-9 relative)
+    rel = ((hb - h_ref).norm() / h_ref.norm()).item()
+    assert rel < 3e-3, rel                       # h is rounded to bf16 once (<= 2^-9 relative)
     y_ref = (hb @ W[2].T) * rw.double()[:, None]
-    rel2 = (acc.double() - y_ref).norm() / y_ref.norm()
-    assert rel2 < 1e-5, rel2                 # f32 accumulation only
-
+    rel2 = ((acc.double() - y_ref).norm() / y_ref.norm()).item()
+    assert rel2 < 2e-5, rel2                     # f32 accumulation only
 
 def _dense(e, d, ff, G, cuda):
     W = []
@@ -197,4 +195,4 @@ def test_w4_grouped_ffn_tcgen05(d, ff, rows, cuda):
         assert rel < 4e-3, (i, rel)
         y_ref = hb @ W2.T
         rel2 = ((y[lo:hi].double() - y_ref).norm() / y_ref.norm()).item()
-        assert rel2 < 1e-5, (i, rel2)
+        assert rel2 < 5e-5, (i, rel2)           # f32 accumulation over K up to 16384
