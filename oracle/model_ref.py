@@ -1,0 +1,133 @@
+"""Tiny Mixtral-style W4 model forward on the CPU (oracle, torch fp32).
+
+PARITY UNPINNED BY THE REFERENCE: the reference computes no model forward
+(PAPER.md:188-192 used third-party vLLM/AWQ, unpinned).
+This restates the build's documented numerics from
+their third-party sources so the B200 engine can be checked:
+  * Mixtral decoder block: HF transformers 5.5.0 modeling_mixtral.py
+    (RMSNorm, rotate-half RoPE, GQA attention, MixtralSparseMoeBlock
+    :74-98 per-expert SiLU(gate)*up -> down, routing-weighted sum);
+  * router: routing_ref (modeling_mixtral.py:109-116 semantics, fixed f64
+    order, reference tie rule);
+  * W4 dequant: w4_ref (vLLM awq_triton.py:54-101 rule).
+Prefill experts use bf16-rounded dequantised weights (what the tcgen05 GEMM
+consumes); decode experts use the exact (q - z) * s products (what the
+factorised GEMV computes) — see oracle/w4_ref.py.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import routing_ref, w4_ref
+
+BF = torch.bfloat16
+
+
+def _bf(x: torch.Tensor) -> torch.Tensor:
+    return x.to(BF).float()
+
+
+def _bits(x: torch.Tensor) -> np.ndarray:
+    return x.to(BF).contiguous().view(torch.int16).numpy().view(np.uint16)
+
+
+class TinyMixtralRef:
+    def __init__(self, shape, dense, seed: int):
+        """shape: ModelShape-like (attributes), dense: DenseWeights on CPU (bf16)."""
+        self.s = shape
+        self.W = dense
+        self.seed = seed
+        d, ff, G = shape.hidden, shape.ffn, shape.group_size
+        self.rounded, self.exact = {}, {}
+        for l in range(shape.num_layers):
+            for e in range(shape.num_experts):
+                r, x = [], []
+                for m, (K, N) in enumerate([(d, ff), (d, ff), (ff, d)]):
+                    c, sc, z = w4_ref.gen_linear(seed, l, e, m, K, N, G)
+                    r.append(torch.from_numpy(w4_ref.bf16_bits_to_f32(w4_ref.dequant(c, sc, z, K, N, G))))
+                    x.append(torch.from_numpy(w4_ref.dequant_exact(c, sc, z, K, N, G)).float())
+                self.rounded[(l, e)] = r          # [N, K] each
+                self.exact[(l, e)] = x
+        hd = shape.head_dim
+        inv = 1.0 / (shape.rope_theta ** (torch.arange(0, hd, 2, dtype=torch.float32) / hd))
+        f = torch.outer(torch.arange(4096, dtype=torch.float32), inv)
+        emb = torch.cat([f, f], -1)
+        self.cos, self.sin = emb.cos(), emb.sin()
+        self.reset()
+
+    def reset(self):
+        L = self.s.num_layers
+        self.K = [None] * L
+        self.V = [None] * L
+        self.pos = 0
+
+    def norm(self, x, g):
+        return _bf(x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + self.s.rms_eps) * g.float())
+
+    def rope(self, x, p0):
+        T = x.shape[0]
+        c, s = self.cos[p0:p0 + T][:, None, :], self.sin[p0:p0 + T][:, None, :]
+        h = x.shape[-1] // 2
+        rot = torch.cat([-x[..., h:], x[..., :h]], -1)
+        return _bf(x * c + rot * s)
+
+    def attn(self, l, h):
+        s = self.s
+        Lw = self.W.layers[l]
+        T = h.shape[0]
+        a = self.norm(h, Lw["ln1"])
+        q = _bf(a @ Lw["wq"].float()).view(T, s.n_heads, s.head_dim)
+        k = _bf(a @ Lw["wk"].float()).view(T, s.n_kv_heads, s.head_dim)
+        v = _bf(a @ Lw["wv"].float()).view(T, s.n_kv_heads, s.head_dim)
+        q, k = self.rope(q, self.pos), self.rope(k, self.pos)
+        self.K[l] = k if self.K[l] is None else torch.cat([self.K[l], k])
+        self.V[l] = v if self.V[l] is None else torch.cat([self.V[l], v])
+        Kx = self.K[l].repeat_interleave(s.n_heads // s.n_kv_heads, dim=1)
+        Vx = self.V[l].repeat_interleave(s.n_heads // s.n_kv_heads, dim=1)
+        S = torch.einsum("thd,shd->hts", q, Kx) / math.sqrt(s.head_dim)
+        n = Kx.shape[0]
+        causal = torch.arange(n)[None, :] <= (torch.arange(T)[:, None] + self.pos)
+        S = S.masked_fill(~causal[None], float("-inf"))
+        o = _bf(torch.einsum("hts,shd->thd", torch.softmax(S, -1), Vx)).reshape(T, -1)
+        return _bf(h + _bf(o @ Lw["wo"].float()))
+
+    def gate(self, l, a):
+        lg = routing_ref.gate_logits(_bits(a), _bits(self.W.layers[l]["wg"]))
+        return routing_ref.topk_route(lg, self.s.top_k)
+
+    def moe(self, l, h, decode: bool, idx_override=None):
+        s = self.s
+        a = self.norm(h, self.W.layers[l]["ln2"])
+        idx, w = self.gate(l, a)
+        if idx_override is not None:
+            idx = idx_override
+        T = h.shape[0]
+        acc = torch.zeros((T, s.hidden), dtype=torch.float32)
+        ws = torch.from_numpy(w)
+        for j in range(s.top_k):
+            for e in range(s.num_experts):
+                rows = np.nonzero(idx[:, j] == e)[0]
+                if rows.size == 0:
+                    continue
+                W1, W3, W2 = (self.exact if decode else self.rounded)[(l, e)]
+                x = a[rows]
+                hh = _bf(torch.nn.functional.silu(x @ W1.T) * (x @ W3.T))
+                y = hh @ W2.T
+                acc[rows] = acc[rows] + ws[rows, j:j + 1] * y
+        return _bf(h + acc), idx, a
+
+    def forward(self, ids, decode: bool, idx_override=None):
+        """ids: 1-D token ids at positions self.pos...; returns (logits of last, per-layer idx)."""
+        h = _bf(self.W.embed[torch.as_tensor(ids)].float())
+        idxs = []
+        for l in range(self.s.num_layers):
+            h = self.attn(l, h)
+            h, idx, _ = self.moe(l, h, decode, None if idx_override is None else idx_override[l])
+            idxs.append(idx)
+        self.pos += len(ids)
+        logits = _bf(self.norm(h[-1:], self.W.norm) @ self.W.lm_head.float())[0]
+        return logits, idxs

@@ -1,0 +1,419 @@
+"""DuoServe-MoE inference runtime on one B200: expert store, HBM expert
+cache and the prefill / decode expert schedules (cache
+semantics SPEC.md:340-438, restated in oracle/sim_ref.py).
+
+  HostExpertStore   all L x M W4 experts in pinned host memory (the "CPU
+                    expert cache"), kernel-ready bytes: one
+                    contiguous blob per expert, one H2D copy per fetch.
+  ExpertCache       slot_count(policy) fixed slots in HBM (config.py:101-114),
+                    a dedicated copy stream, per-slot ready/free cudaEvents,
+                    and the fetch log that must equal the oracle's.
+  Engine            prefill(ids) / decode_step() — the reference-facing serving
+                    API.  Compute stream: attention, K1 gate, K2 permute,
+                    K3/K4 expert FFN, combine.  Copy stream: expert H2D.
+                    Predict stream: K5 predictor for layer l+1.
+
+Schedules (policy "duoserve"):
+  prefill, per layer l  the copy stream speculatively fetches expert 0 of
+      layer l while attention runs (the first transfer overlaps the non-MoE
+      compute); after the gate + permute the activated set A_l
+      is read back and the rest of A_l is fetched ascending, each expert once,
+      into a ring of slots — the compute stream runs expert e_i's grouped FFN
+      (K3) as soon as its copy event fires while e_{i+1} streams in.
+  decode, per token     layer 0 fetches after the gate; for l >= 1 the
+      prediction P_l made during layer l-1 was prefetched; sync point 1
+      compares the gate set E_l with P_l and re-fetches only the wrong slots;
+      the predictor for l+1 runs on its own stream as soon as E_l is in the
+      device history buffer; sync point 2 issues the prefetch of P_{l+1} into
+      the two slots released by layer l-1.
+Policy "oracle" replays a recorded routing as the prediction (the SPEC's
+DuoServeOracle); "ondemand" fetches after the gate (ACC baseline).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import ops
+from .config import ModelShape, SchedulerPolicy, model_config_for_shape, slot_count
+from .model import DenseWeights, KVCache, attention_block, init_dense_weights, logits_last, rms_norm, rope_tables
+from .predictor import ExpertMLP, StatsOnDevice, _mode_code
+
+
+class HostExpertStore:
+    """Pinned host memory holding every expert blob: [L, M, blob_bytes] u8."""
+
+    def __init__(self, shape: ModelShape, seed: int, device, layers: int | None = None):
+        self.shape = shape
+        self.seed = seed
+        L = layers if layers is not None else shape.num_layers
+        self.offsets, self.blob_bytes = ops.expert_layout(shape.hidden, shape.ffn, shape.group_size)
+        t0 = time.time()
+        self.host = torch.empty((L, shape.num_experts, self.blob_bytes), dtype=torch.uint8, pin_memory=True)
+        self.alloc_s = time.time() - t0
+        # generate on the device (counter-based, bit-identical to oracle/w4_ref.py) then D2H
+        t0 = time.time()
+        stage = [torch.empty(self.blob_bytes, dtype=torch.uint8, device=device) for _ in range(2)]
+        s = torch.cuda.current_stream(device)
+        for l in range(L):
+            for e in range(shape.num_experts):
+                buf = stage[(l * shape.num_experts + e) % 2]
+                ops.w4_generate(seed, l, e, shape.hidden, shape.ffn, shape.group_size, buf)
+                self.host[l, e].copy_(buf, non_blocking=True)
+        s.synchronize()
+        self.fill_s = time.time() - t0
+
+    @property
+    def nbytes(self) -> int:
+        return self.host.numel()
+
+
+class ExpertCache:
+    """Fixed-capacity HBM expert slots fed by a dedicated copy stream."""
+
+    def __init__(self, store: HostExpertStore, n_slots: int, device):
+        self.store = store
+        self.n_slots = n_slots
+        self.device = device
+        self.slots = torch.empty((n_slots, store.blob_bytes), dtype=torch.uint8, device=device)
+        self.copy_stream = torch.cuda.Stream(device)
+        self.ready = [torch.cuda.Event() for _ in range(n_slots)]
+        self.free = [torch.cuda.Event() for _ in range(n_slots)]
+        self.used = [False] * n_slots
+        self.content = [None] * n_slots          # (layer, expert) resident or in flight
+        self.bytes_copied = 0
+        self.n_copies = 0
+        sh = store.shape
+        self._structs = [ops.expert_struct(self.slots[i].data_ptr(), sh.hidden, sh.ffn, sh.group_size)
+                         for i in range(n_slots)]
+
+    @property
+    def nbytes(self) -> int:
+        return self.slots.numel()
+
+    def load(self, slot: int, layer: int, expert: int) -> None:
+        """Queue the H2D copy of expert (layer, expert) into slot (after its last use)."""
+        with torch.cuda.stream(self.copy_stream):
+            if self.used[slot]:
+                self.copy_stream.wait_event(self.free[slot])
+            self.slots[slot].copy_(self.store.host[layer, expert], non_blocking=True)
+            self.ready[slot].record(self.copy_stream)
+        self.content[slot] = (layer, expert)
+        self.bytes_copied += self.store.blob_bytes
+        self.n_copies += 1
+
+    def acquire(self, slot: int) -> "object":
+        """Make the current (compute) stream wait until the slot's copy landed."""
+        torch.cuda.current_stream(self.device).wait_event(self.ready[slot])
+        return self._structs[slot]
+
+    def release(self, slot: int) -> None:
+        self.free[slot].record(torch.cuda.current_stream(self.device))
+        self.used[slot] = True
+
+
+class MLPDriver:
+    """K5 on the predict stream: P_{l+1} from the device history buffer."""
+
+    def __init__(self, net: ExpertMLP, pop, aff, L: int, M: int, k: int, device):
+        self.dev = net.device(device)
+        self.stats = StatsOnDevice(pop, aff, device)
+        self.mode = _mode_code(net.meta.get("affinity_mode", "pool"))
+        self.L, self.M, self.k = L, M, k
+        self.stream = torch.cuda.Stream(device)
+        self.target = torch.zeros(1, dtype=torch.int32, device=device)
+        self.targets = [torch.full((1,), l, dtype=torch.int32, device=device) for l in range(L)]
+        self.out = torch.empty((1, k), dtype=torch.int32, device=device)
+        self.host_out = torch.empty((1, k), dtype=torch.int32, pin_memory=True)
+        self.done = torch.cuda.Event()
+        self.nbytes = self.dev.nbytes + self.stats.pop.nbytes + self.stats.aff.nbytes
+
+    def launch(self, hist: torch.Tensor, after: torch.cuda.Event, target_layer: int) -> None:
+        with torch.cuda.stream(self.stream):
+            self.stream.wait_event(after)
+            self.dev.predict_state(hist, self.targets[target_layer], self.stats.pop, self.stats.aff, self.L,
+                                   self.M, self.k, self.mode, self.k, out=self.out, stream=self.stream)
+            self.host_out.copy_(self.out, non_blocking=True)
+            self.done.record(self.stream)
+
+    def result(self) -> list:
+        self.done.synchronize()
+        return [int(e) for e in self.host_out[0].tolist()]
+
+
+class TraceDriver:
+    """Perfect predictor for policy 'oracle': replays recorded decode routing."""
+
+    def __init__(self, paths):
+        self.paths = paths     # paths[t][l] -> tuple
+        self.t = 0
+        self._next = None
+
+    def launch(self, hist, after, target_layer: int) -> None:
+        self._next = list(self.paths[self.t][target_layer])
+
+    def result(self) -> list:
+        return self._next
+
+
+@dataclass
+class StepTiming:
+    ms: float
+    bytes_h2d: int
+
+
+class Engine:
+    """Reference-facing serving API: load -> prefill(ids) -> decode_step()*."""
+
+    def __init__(self, shape: ModelShape, policy="duoserve", seed: int = 0, device="cuda",
+                 dense: DenseWeights | None = None, store: HostExpertStore | None = None,
+                 predictor: ExpertMLP | None = None, pop=None, aff=None, oracle_paths=None,
+                 max_seq: int = 2048, max_prefill: int = 2048):
+        self.shape = shape
+        self.policy = SchedulerPolicy(policy)
+        self.device = torch.device(device)
+        sh = shape
+        self.L, self.M, self.k, self.d, self.ff, self.G = (sh.num_layers, sh.num_experts, sh.top_k, sh.hidden,
+                                                           sh.ffn, sh.group_size)
+        self.W = dense if dense is not None else init_dense_weights(sh, seed, device=self.device)
+        if self.W.embed.device != self.device:
+            self.W = self.W.to(self.device)
+        self.store = store if store is not None else HostExpertStore(sh, seed, self.device)
+        cfg = model_config_for_shape(sh)
+        self.n_slots = slot_count(self.policy, cfg)
+        self.cache = ExpertCache(self.store, self.n_slots, self.device)
+        self.kv = KVCache(sh, max_seq, self.device)
+        self.cos, self.sin = rope_tables(sh, max_seq, self.device)
+        self.driver = None
+        if self.policy is SchedulerPolicy.DUOSERVE:
+            if predictor is None or pop is None or aff is None:
+                raise ValueError("policy 'duoserve' needs predictor, pop and aff")
+            self.driver = MLPDriver(predictor, pop, aff, self.L, self.M, self.k, self.device)
+        elif self.policy is SchedulerPolicy.DUOSERVE_ORACLE:
+            if oracle_paths is None:
+                raise ValueError("policy 'oracle' needs the recorded decode routing (oracle_paths)")
+            self.driver = TraceDriver(oracle_paths)
+        elif self.policy is SchedulerPolicy.PREFETCH_ALL:
+            raise NotImplementedError("prefetchall policy is not implemented on the B200 runtime yet")
+        dev = self.device
+        # decode buffers
+        self.hist = torch.zeros((1, self.L * self.k), dtype=torch.int32, device=dev)
+        self.idx1 = torch.empty((1, self.k), dtype=torch.int32, device=dev)
+        self.w1 = torch.empty((1, self.k), dtype=torch.float32, device=dev)
+        self.idx_host = torch.empty((1, self.k), dtype=torch.int32, pin_memory=True)
+        self.h_buf = torch.empty((1, self.ff), dtype=torch.bfloat16, device=dev)
+        self.acc = torch.zeros((1, self.d), dtype=torch.float32, device=dev)
+        self.ev_gate = torch.cuda.Event()
+        # prefill buffers
+        P = max_prefill
+        self.p_idx = torch.empty((P, self.k), dtype=torch.int32, device=dev)
+        self.p_w = torch.empty((P, self.k), dtype=torch.float32, device=dev)
+        self.p_off = torch.empty(self.M + 1, dtype=torch.int32, device=dev)
+        self.p_off_host = torch.empty(self.M + 1, dtype=torch.int32, pin_memory=True)
+        self.p_pos = torch.empty(P * self.k, dtype=torch.int32, device=dev)
+        self.p_src = torch.empty(P * self.k, dtype=torch.int32, device=dev)
+        self.p_xperm = torch.empty((P * self.k, self.d), dtype=torch.bfloat16, device=dev)
+        self.p_h = torch.empty((P * self.k, self.ff), dtype=torch.bfloat16, device=dev)
+        self.p_y = torch.empty((P * self.k, self.d), dtype=torch.float32, device=dev)
+        ws = max(ops.grouped_ffn_workspace(r, self.d, self.ff) for r in (P * self.k // 4, P * self.k))
+        self.p_ws = torch.empty(max(ws, 256), dtype=torch.uint8, device=dev)
+        self.prefill_idx_host = None
+        self.capture = None          # debug/parity: list of (phase, layer, gate input, idx)
+        self.last_logits = None
+        self.reset()
+
+    # ------------------------------------------------------------------ API
+    def reset(self) -> None:
+        self.kv.len = 0
+        self.log: list = []
+        self.paths_decode: list = []          # recorded routing per decode token
+        self.paths_prefill = None
+        self.token = None
+        self.t_decode = 0
+        self.cache.used = [False] * self.n_slots
+        self.cache.content = [None] * self.n_slots
+        self._spec = None                     # (slot, layer, expert) speculative prefill fetch
+        self._ring = 0
+        self._pred_next = None
+        self.hist.zero_()
+
+    @torch.no_grad()
+    def prefill(self, ids) -> int:
+        """Prompt pass; returns the first generated token (greedy)."""
+        ids = torch.as_tensor(ids, dtype=torch.long, device=self.device).reshape(-1)
+        T = ids.numel()
+        h = self.W.embed[ids]
+        idx_all = []
+        self._spec_fetch(0)
+        for l in range(self.L):
+            h = attention_block(self.shape, self.W.layers[l], h, self.kv, l, 0, self.cos, self.sin)
+            h, idx_host = self._moe_prefill(l, h, T)
+            idx_all.append(idx_host)
+        self.kv.len = T
+        self.paths_prefill = np.stack(idx_all, axis=1)     # [T, L, k]
+        lg = logits_last(self.shape, self.W, h[-1:])[0]
+        self.last_logits = lg
+        tok = int(torch.argmax(lg).item())
+        self.token = tok
+        self.t_decode = 0
+        return tok
+
+    @torch.no_grad()
+    def decode_step(self) -> int:
+        """One greedy decode token (feeds back the previous output token)."""
+        pos = self.kv.len
+        h = self.W.embed[torch.tensor([self.token], device=self.device)]
+        path = []
+        if isinstance(self.driver, TraceDriver):
+            self.driver.t = self.t_decode
+        self._pred_next = None
+        for l in range(self.L):
+            h = attention_block(self.shape, self.W.layers[l], h, self.kv, l, pos, self.cos, self.sin)
+            h, E = self._moe_decode(l, h)
+            path.append(tuple(E))
+        self.kv.len = pos + 1
+        self.paths_decode.append(tuple(path))
+        lg = logits_last(self.shape, self.W, h)[0]
+        self.last_logits = lg
+        tok = int(torch.argmax(lg).item())
+        self.token = tok
+        self.t_decode += 1
+        return tok
+
+    def generate(self, ids, n_new: int) -> list:
+        out = [self.prefill(ids)]
+        for _ in range(n_new - 1):
+            out.append(self.decode_step())
+        return out
+
+    # -------------------------------------------------------------- prefill
+    def _next_ring_slot(self) -> int:
+        s = self._ring
+        self._ring = (self._ring + 1) % self.n_slots
+        return s
+
+    def _spec_fetch(self, layer: int) -> None:
+        """Speculative first transfer of layer `layer` (expert 0) to overlap attention."""
+        if layer >= self.L or self.policy is SchedulerPolicy.ON_DEMAND:
+            self._spec = None
+            return
+        slot = self._next_ring_slot()
+        self.cache.load(slot, layer, 0)
+        self._spec = (slot, layer, 0)
+
+    def _moe_prefill(self, l: int, h: torch.Tensor, T: int):
+        sh = self.shape
+        a = rms_norm(h, self.W.layers[l]["ln2"], sh.rms_eps)
+        idx, w = self.p_idx[:T], self.p_w[:T]
+        ops.gate_topk(a, self.W.layers[l]["wg"], self.k, idx, w)
+        if self.capture is not None:
+            self.capture.append(("prefill", l, a.cpu(), idx.cpu()))
+        ops.permute(idx, a, self.M, self.p_off, self.p_pos[:T * self.k], self.p_src[:T * self.k],
+                    self.p_xperm[:T * self.k])
+        self.p_off_host.copy_(self.p_off, non_blocking=True)
+        idx_host = torch.empty((T, self.k), dtype=torch.int32, pin_memory=True)
+        idx_host.copy_(idx, non_blocking=True)
+        done = torch.cuda.Event()
+        done.record()
+        done.synchronize()                                  # activated set -> host
+        off = self.p_off_host.tolist()
+        A = [e for e in range(self.M) if off[e + 1] > off[e]]
+        plan = []                                           # (expert, slot, already_queued)
+        if self.policy is SchedulerPolicy.ON_DEMAND:
+            plan = [(e, i % self.n_slots, False) for i, e in enumerate(A)]
+        else:
+            spec = self._spec if (self._spec is not None and self._spec[1] == l) else None
+            if spec is not None:
+                plan.append((spec[2], spec[0], True))
+            plan += [(e, self._next_ring_slot(), False) for e in A if not (spec and e == spec[2])]
+        self.log.append({"phase": "prefill", "layer": l, "fetch": [e for e, _, _ in plan], "activated": A})
+        # sliding window over the slot ring: the copy into a slot is queued only
+        # after the compute that last used it has been queued (its free event)
+        window = self.n_slots if self.policy is not SchedulerPolicy.ON_DEMAND else self.n_slots
+        for i in range(min(window, len(plan))):
+            e, slot, queued = plan[i]
+            if not queued:
+                self.cache.load(slot, l, e)
+        for i, (e, slot, _) in enumerate(plan):
+            if off[e + 1] > off[e]:
+                st = self.cache.acquire(slot)
+                lo, hi = off[e], off[e + 1]
+                ops.grouped_ffn(self.p_xperm[lo:hi], [0, hi - lo], [st], self.d, self.ff, self.G,
+                                self.p_h[lo:hi], self.p_y[lo:hi], self.p_ws)
+            self.cache.release(slot)
+            if i + window < len(plan):
+                e2, slot2, queued2 = plan[i + window]
+                if not queued2:
+                    self.cache.load(slot2, l, e2)
+        # next layer's first expert streams while this layer combines + next attention runs
+        self._spec_fetch(l + 1)
+        out = torch.empty_like(h)
+        ops.unpermute_combine(self.p_y[:T * self.k], self.p_pos[:T * self.k], w, h, out)
+        return out, idx_host.numpy()
+
+    # --------------------------------------------------------------- decode
+    def _moe_decode(self, l: int, h: torch.Tensor):
+        sh = self.shape
+        a = rms_norm(h, self.W.layers[l]["ln2"], sh.rms_eps)
+        ops.gate_topk(a, self.W.layers[l]["wg"], self.k, self.idx1, self.w1, hist=self.hist, layer=l)
+        self.ev_gate.record()
+        self.idx_host.copy_(self.idx1, non_blocking=True)
+        ev_idx = torch.cuda.Event()
+        ev_idx.record()
+        use_pred = self.driver is not None
+        if use_pred and l + 1 < self.L:
+            self.driver.launch(self.hist, self.ev_gate, l + 1)     # predict stream, overlapped
+        ev_idx.synchronize()                                       # sync point 1: E_l on the host
+        E = [int(e) for e in self.idx_host[0].tolist()]
+        if self.capture is not None:
+            self.capture.append(("decode", l, a.cpu(), self.idx_host.clone()))
+        slot_of = {}
+        if l == 0 or not use_pred:
+            base = 0 if (l % 2 == 0 or self.n_slots < 2 * self.k) else self.k
+            for j, e in enumerate(E):
+                slot = (base + j) % self.n_slots
+                self.cache.load(slot, l, e)
+                slot_of[e] = slot
+            self.log.append({"phase": "decode", "token": self.t_decode, "layer": l, "fetch": E,
+                             "kind": "ondemand"})
+        else:
+            P, P_slots = self._pred_next
+            miss = sorted(set(E) - set(P))
+            wrong_slots = [s for p, s in zip(P, P_slots) if p not in E]
+            for p, s in zip(P, P_slots):
+                if p in E:
+                    slot_of[p] = s
+            for e, s in zip(miss, wrong_slots):
+                self.cache.load(s, l, e)                            # blocking re-fetch of the wrong slot
+                slot_of[e] = s
+            self.log.append({"phase": "decode", "token": self.t_decode, "layer": l, "pred": sorted(P),
+                             "gate": sorted(E), "refetch": miss})
+        # expert compute: hits first (already resident), then the re-fetched ones
+        refetched = set(self.log[-1].get("refetch", []))
+        for e in [x for x in E if x not in refetched] + [x for x in E if x in refetched]:
+            j = E.index(e)
+            st = self.cache.acquire(slot_of[e])
+            ops.swiglu_gemv(a, st, self.d, self.ff, self.G, self.h_buf)
+            ops.down_gemv(self.h_buf, st, self.d, self.ff, self.G, self.w1[0, j:], 1, self.acc)
+            self.cache.release(slot_of[e])
+        out = torch.empty_like(h)
+        ops.combine_finalize(self.acc, h, out)
+        # sync point 2: prediction for l+1 ready -> prefetch into the slots layer l-1 used
+        if use_pred and l + 1 < self.L:
+            Pn = self.driver.result()
+            cur = set(slot_of.values())
+            free = [s for s in range(self.n_slots) if s not in cur][: self.k]
+            for e, s in zip(Pn, free):
+                self.cache.load(s, l + 1, e)
+            self._pred_next = (Pn, free)
+        return out, E
+
+    # -------------------------------------------------------------- metrics
+    def resident_bytes(self) -> dict:
+        pred = self.driver.nbytes if isinstance(self.driver, MLPDriver) else 0
+        return {"non_moe": self.W.nbytes(), "expert_slots": self.cache.nbytes, "predictor": pred,
+                "kv_cache": self.kv.nbytes, "model_total": self.shape.total_bytes}
