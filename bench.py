@@ -1,0 +1,368 @@
+#!/usr/bin/env python
+"""Benchmark: Mixtral-8x7B-shaped W4 e2e latency (TTFT, decode tok/s) at
+<= 15 % expert residency (BASELINE.json metric, configs[1]: batch 1, prefill
+512 + decode 128, 1 x B200, random-init weights, synthetic prompt ids).
+
+One "step" = one request through the public serving API: Engine.prefill
+(512 prompt tokens) + 128 Engine.decode_step() calls, with the DuoServe
+schedule (2k = 4 expert slots in HBM, all 256 experts streamed from pinned
+host memory; predictor-driven decode prefetch).
+
+    python bench.py [--steps K] [--warmup W] [--gpus N] [--config mixtral-8x7b]
+    python bench.py --impl reference      # CPU oracle port of the reference path
+
+Under torchrun (N > 1) every rank serves an independent replica (the path is
+single-GPU by design; expert-parallel 8x22B is a separate
+extension): scaling "weak", the time is the max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "Mixtral-8x7B W4 e2e latency (TTFT, decode tok/s) at 15% expert residency"
+UNIT = "ms/request (prefill 512 + decode 128, batch 1)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="mixtral-8x7b")
+    ap.add_argument("--policy", default="duoserve", choices=["duoserve", "oracle", "ondemand"])
+    ap.add_argument("--prefill", type=int, default=512)
+    ap.add_argument("--decode", type=int, default=128)
+    ap.add_argument("--warmup-decode", type=int, default=None,
+                    help="decode tokens per warm-up step (default: same as --decode)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--out", default=None, help="also write the JSON line to this file")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- helpers
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.p.kill()
+
+    def summary(self) -> dict:
+        self.f.flush()
+        rows = []
+        for line in Path(self.f.name).read_text().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
+        loaded = [s for s in sm if mx and s > 0.5 * max(mx)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws <= 1:
+        return 0, 1, 0
+    import torch
+    import torch.distributed as dist
+    lr = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(lr)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
+    return dist.get_rank(), ws, lr
+
+
+def measured_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text())
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "_fallback": True}
+
+
+def predictor_inputs(shape, seed: int = 0):
+    """ExpertMLP(d_in, 8, seed=0) + pop/aff from generate_traces(default_generator_params(L, 8, 0.8, seed=7))
+    (SURVEY.md §8d)."""
+    from paper_2509_07379_b200 import config as C, predictor as P, stats as S, trace as T
+    cfg = C.model_config_for_shape(shape)
+    ds = T.generate_traces(T.default_generator_params(shape.num_layers, shape.num_experts, 0.8, seed=7), cfg,
+                           n_requests=4, decode_len=16, prefill_len=16)
+    pop, aff = S.build_popularity(ds), S.build_affinity(ds)
+    net = P.ExpertMLP(P.feature_length(shape.num_layers, shape.num_experts, shape.top_k), shape.num_experts,
+                      seed=seed, meta={"L": shape.num_layers, "M": shape.num_experts, "k": shape.top_k,
+                                       "affinity_mode": "pool"})
+    return net, pop, aff
+
+
+# ------------------------------------------------------------- CPU baseline
+def cpu_reference_sample(shape, prefill: int, budget_s: float = 20.0) -> dict:
+    """The reference path on the host cores (oracle port): one MoE layer of
+    the request — prefill gate + grouped W4 expert FFN of 512 tokens, one
+    decode token's gate + 2-expert FFN + the reference predictor step
+    (construct_input + ExpertMLP eval + topk, predictor.py:80-106/197-232/419-421)
+    — timed and scaled by L layers and 128 decode tokens."""
+    import numpy as np
+    import torch
+    from oracle import predictor_ref, routing_ref, w4_ref
+    threads = os.cpu_count() or 1
+    torch.set_num_threads(threads)
+    d, ff, G, M, k, L = shape.hidden, shape.ffn, shape.group_size, shape.num_experts, shape.top_k, shape.num_layers
+    rng = np.random.default_rng(0)
+    # weights of one layer (generation is not timed)
+    experts = []
+    for e in range(M):
+        experts.append([torch.from_numpy(w4_ref.bf16_bits_to_f32(
+            w4_ref.dequant(*w4_ref.gen_linear(0, 0, e, m, K, N, G), K, N, G))) for m, (K, N) in
+            enumerate([(d, ff), (d, ff), (ff, d)])])
+    wg = (rng.standard_normal((M, d)) * 0.02).astype(np.float32)
+    wg_bits = w4_ref.bf16_round_bits(wg)
+    x = w4_ref.bf16_round_bits(rng.standard_normal((prefill, d)).astype(np.float32))
+    net = predictor_ref.RefNet(predictor_ref_dim(shape), M, (2048, 1024, 512, 256, 128, 64), 0)
+    pop = np.full((L, M), 1.0 / M)
+    aff = np.full((L - 1, M, M), 1.0 / M)
+    path = tuple(tuple(sorted(rng.choice(M, k, replace=False).tolist())) for _ in range(L))
+
+    def moe(xb, rows_idx):
+        xt = torch.from_numpy(w4_ref.bf16_bits_to_f32(xb))
+        out = torch.zeros(xt.shape[0], d)
+        for e in range(M):
+            rows = np.nonzero((rows_idx == e).any(axis=1))[0]
+            if rows.size:
+                W1, W3, W2 = experts[e]
+                xr = xt[rows]
+                h = torch.nn.functional.silu(xr @ W1.T) * (xr @ W3.T)
+                out[rows] += h @ W2.T
+        return out
+
+    t0 = time.perf_counter()
+    lg = routing_ref.gate_logits(x, wg_bits)
+    idx, _ = routing_ref.topk_route(lg, k)
+    moe(x, idx)
+    t_prefill_layer = time.perf_counter() - t0
+    reps = 0
+    t0 = time.perf_counter()
+    while True:
+        lg = routing_ref.gate_logits(x[:1], wg_bits)
+        idx, _ = routing_ref.topk_route(lg, k)
+        moe(x[:1], idx)
+        feats = predictor_ref.features(path, min(5, L - 1), pop, aff)
+        predictor_ref.topk_indices(net.forward(feats), k)
+        reps += 1
+        if time.perf_counter() - t0 > min(budget_s, 5.0) or reps >= 20:
+            break
+    t_decode_layer = (time.perf_counter() - t0) / reps
+    ttft_ms = 1e3 * t_prefill_layer * L
+    tok_ms = 1e3 * t_decode_layer * L
+    return {"ttft_ms": ttft_ms, "decode_ms_per_token": tok_ms, "cores": threads,
+            "sample": (f"1 of {L} MoE layers at {shape.name} shape: prefill {prefill} tokens "
+                       f"(gate + grouped W4 SwiGLU FFN, torch fp32 on dequantised weights) and "
+                       f"{reps} decode tokens (gate + 2 experts + reference predictor step), scaled x{L} layers")}
+
+
+def predictor_ref_dim(shape):
+    return shape.num_layers * shape.top_k + 2 * shape.num_experts + 1
+
+
+# ------------------------------------------------------------------ arms
+def run_reference(args):
+    rank, ws, _ = dist_init()
+    if rank != 0:
+        return
+    from paper_2509_07379_b200.config import load_shape
+    shape = load_shape(args.config)
+    vals = []
+    samp = None
+    for i in range(args.warmup + args.steps):
+        r = cpu_reference_sample(shape, args.prefill)
+        if i >= args.warmup:
+            vals.append(r["ttft_ms"] + args.decode * r["decode_ms_per_token"])
+            samp = r
+    v = statistics.median(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 1), "unit": UNIT, "n_gpus": 0,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(v, 1), "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{shape.name} W4 random-init, batch 1, prefill {args.prefill} + decode "
+                                   f"{args.decode}", "prefill": args.prefill, "decode": args.decode},
+            "ttft_ms": round(samp["ttft_ms"], 1),
+            "decode_tok_s": round(1e3 / samp["decode_ms_per_token"], 3),
+            "cpu_baseline": {"value": round(v, 1), "unit": UNIT, "cores": samp["cores"], "kind": "port",
+                             "sample": samp["sample"]},
+            "e2e": {"value": round(v, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    rank, ws, lr = dist_init()
+    dev = torch.device("cuda", lr)
+    torch.cuda.set_device(dev)
+    from paper_2509_07379_b200 import _lib
+    _lib.load()                          # fail loudly if the CUDA library is missing
+    from paper_2509_07379_b200.config import load_shape
+    from paper_2509_07379_b200.engine import Engine
+    shape = load_shape(args.config)
+    t_setup = time.time()
+    net, pop, aff = predictor_inputs(shape) if args.policy == "duoserve" else (None, None, None)
+    eng = Engine(shape, args.policy if args.policy != "oracle" else "duoserve", seed=args.seed, device=dev,
+                 predictor=net, pop=pop, aff=aff, max_seq=args.prefill + args.decode + 8,
+                 max_prefill=args.prefill)
+    gen = torch.Generator().manual_seed(args.seed + 1000 * rank)
+    ids_host = torch.randint(0, shape.vocab, (args.prefill,), generator=gen).pin_memory()
+    if args.policy == "oracle":
+        # record the routing once, then replay it as the perfect predictor (SPEC DuoServeOracle)
+        eng.reset()
+        eng.generate(ids_host, args.decode + 1)
+        paths = eng.paths_decode
+        eng = Engine(shape, "oracle", seed=args.seed, device=dev, dense=eng.W, store=eng.store,
+                     oracle_paths=paths, max_seq=args.prefill + args.decode + 8, max_prefill=args.prefill)
+    setup_s = time.time() - t_setup
+    prof = eng.enable_profile()
+
+    def one_step(n_decode: int):
+        eng.reset()
+        c0 = eng.cache.bytes_copied
+        s = torch.cuda.current_stream()
+        e0, e1, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True), \
+            torch.cuda.Event(enable_timing=True)
+        w0 = time.perf_counter()
+        e0.record(s)
+        ids = ids_host.to(dev, non_blocking=True)       # H2D of the prompt inside the step
+        tok0 = eng.prefill(ids)                          # returns a host int (D2H)
+        e1.record(s)
+        w1 = time.perf_counter()
+        toks = [tok0]
+        for _ in range(n_decode):
+            toks.append(eng.decode_step())
+        e2.record(s)
+        torch.cuda.synchronize()
+        w2 = time.perf_counter()
+        return {"ttft_ms": e0.elapsed_time(e1), "decode_ms": e1.elapsed_time(e2),
+                "e2e_wall_ms": 1e3 * (w2 - w0), "ttft_wall_ms": 1e3 * (w1 - w0),
+                "h2d_experts": eng.cache.bytes_copied - c0, "tokens": toks,
+                "d2h": eng.d2h_bytes}
+
+    wd = args.warmup_decode if args.warmup_decode is not None else args.decode
+    for _ in range(args.warmup):
+        one_step(wd)
+    prof.reset()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    res = []
+    with ClockSampler(lr) as clk:
+        for _ in range(args.steps):
+            res.append(one_step(args.decode))
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    ms_step = statistics.median(r["ttft_ms"] + r["decode_ms"] for r in res)
+    e2e_ms = statistics.median(r["e2e_wall_ms"] for r in res)
+    if ws > 1:
+        t = torch.tensor([ms_step, e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step, e2e_ms = t.tolist()
+    if rank != 0:
+        return
+    r0 = res[len(res) // 2]
+    ttft = statistics.median(r["ttft_ms"] for r in res)
+    dec_ms = statistics.median(r["decode_ms"] for r in res)
+    peaks = measured_peaks()
+    link_gbs = eng.link_peak_gbs()
+    h2d_step = r0["h2d_experts"] + args.prefill * 8
+    kern = prof.summary(peaks)
+    res_b = eng.resident_bytes()
+    peak_dev = torch.cuda.max_memory_allocated(dev)
+    line = {
+        "metric": METRIC, "value": round(ms_step, 1), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 1), "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16 activations, W4 (int4 g128) experts, f32 accumulate",
+        "data": "synthetic (random-init W4 experts from a counter-based generator, random prompt ids)",
+        "config": {"workload": f"{shape.name}-shaped W4, batch 1, prefill {args.prefill} + decode {args.decode}, "
+                               f"1 request per GPU, policy {args.policy}",
+                   "model": shape.name, "global_batch": ws, "seq_len": args.prefill + args.decode,
+                   "parallelism": f"replicas{ws}" if ws > 1 else "single-gpu",
+                   "expert_slots": eng.n_slots,
+                   "l2": "inputs > L2: every expert byte is streamed from pinned host memory per request"},
+        "ttft_ms": round(ttft, 2), "decode_tok_s": round(args.decode / (dec_ms / 1e3), 3),
+        "decode_ms_per_token": round(dec_ms / args.decode, 3),
+        "residency": {"peak_device_bytes": int(peak_dev), "model_bytes": int(shape.total_bytes),
+                      "fraction": round(peak_dev / shape.total_bytes, 4), **{k: int(v) for k, v in res_b.items()}},
+        "link": {"h2d_bytes_per_request": int(r0["h2d_experts"]),
+                 "achieved_gbs": round(r0["h2d_experts"] / ((ttft + dec_ms) / 1e3) / 1e9, 2),
+                 "peak_gbs_measured": round(link_gbs, 2),
+                 "frac": round(r0["h2d_experts"] / ((ttft + dec_ms) / 1e3) / 1e9 / link_gbs, 3),
+                 "ttft_floor_ms": round(eng.prefill_bytes_floor() / link_gbs / 1e6, 1),
+                 "decode_floor_ms_per_token": round(eng.decode_bytes_floor() / link_gbs / 1e6, 2)},
+        "roofline": kern["dominant"],
+        "kernels": kern["all"],
+        "gpu_launches": kern["launches"],
+        "e2e": {"value": round(e2e_ms, 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d_step),
+                "d2h_bytes_per_step": int(r0["d2h"])},
+        "clocks": clk.summary(),
+        "setup_s": round(setup_s, 1),
+        "predictor": eng.hit_summary(),
+    }
+    if not args.no_cpu_baseline and ws == 1:
+        cb = cpu_reference_sample(shape, args.prefill)
+        v = cb["ttft_ms"] + args.decode * cb["decode_ms_per_token"]
+        line["cpu_baseline"] = {"value": round(v, 1), "unit": UNIT, "cores": cb["cores"], "kind": "port",
+                                "sample": cb["sample"]}
+    out = json.dumps(line)
+    print(out)
+    if args.out:
+        Path(args.out).write_text(out + "\n")
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

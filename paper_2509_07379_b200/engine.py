@@ -223,6 +223,9 @@ class Engine:
         self.p_ws = torch.empty(max(ws, 256), dtype=torch.uint8, device=dev)
         self.prefill_idx_host = None
         self.capture = None          # debug/parity: list of (phase, layer, gate input, idx)
+        self.prof = None             # KernelProfiler when enabled (bench)
+        self.d2h_bytes = 0
+        self._link_peak = None
         self.last_logits = None
         self.reset()
 
@@ -240,6 +243,11 @@ class Engine:
         self._ring = 0
         self._pred_next = None
         self.hist.zero_()
+        self.d2h_bytes = 0
+
+    def enable_profile(self) -> "KernelProfiler":
+        self.prof = KernelProfiler()
+        return self.prof
 
     @torch.no_grad()
     def prefill(self, ids) -> int:
@@ -320,6 +328,7 @@ class Engine:
         done = torch.cuda.Event()
         done.record()
         done.synchronize()                                  # activated set -> host
+        self.d2h_bytes += self.p_off_host.nbytes + idx_host.nbytes
         off = self.p_off_host.tolist()
         A = [e for e in range(self.M) if off[e + 1] > off[e]]
         plan = []                                           # (expert, slot, already_queued)
@@ -342,8 +351,12 @@ class Engine:
             if off[e + 1] > off[e]:
                 st = self.cache.acquire(slot)
                 lo, hi = off[e], off[e + 1]
+                ev = self.prof.start() if self.prof else None
                 ops.grouped_ffn(self.p_xperm[lo:hi], [0, hi - lo], [st], self.d, self.ff, self.G,
                                 self.p_h[lo:hi], self.p_y[lo:hi], self.p_ws)
+                if self.prof:
+                    self.prof.stop("K3 w4_grouped_ffn (tcgen05)", ev, self.store.blob_bytes,
+                                   6.0 * (hi - lo) * self.d * self.ff)
             self.cache.release(slot)
             if i + window < len(plan):
                 e2, slot2, queued2 = plan[i + window]
@@ -368,6 +381,7 @@ class Engine:
         if use_pred and l + 1 < self.L:
             self.driver.launch(self.hist, self.ev_gate, l + 1)     # predict stream, overlapped
         ev_idx.synchronize()                                       # sync point 1: E_l on the host
+        self.d2h_bytes += self.idx_host.nbytes + (4 * self.k if use_pred else 0)
         E = [int(e) for e in self.idx_host[0].tolist()]
         if self.capture is not None:
             self.capture.append(("decode", l, a.cpu(), self.idx_host.clone()))
@@ -397,8 +411,11 @@ class Engine:
         for e in [x for x in E if x not in refetched] + [x for x in E if x in refetched]:
             j = E.index(e)
             st = self.cache.acquire(slot_of[e])
+            ev = self.prof.start() if self.prof else None
             ops.swiglu_gemv(a, st, self.d, self.ff, self.G, self.h_buf)
             ops.down_gemv(self.h_buf, st, self.d, self.ff, self.G, self.w1[0, j:], 1, self.acc)
+            if self.prof:
+                self.prof.stop("K4 w4_swiglu_gemv+down_gemv", ev, self.store.blob_bytes)
             self.cache.release(slot_of[e])
         out = torch.empty_like(h)
         ops.combine_finalize(self.acc, h, out)
@@ -413,7 +430,97 @@ class Engine:
         return out, E
 
     # -------------------------------------------------------------- metrics
+    def link_peak_gbs(self) -> float:
+        """Measured pinned H2D bandwidth (copy engine), 1 expert blob x 16."""
+        if self._link_peak is None:
+            src = self.store.host[0, 0]
+            dst = self.cache.slots[0]
+            s = self.cache.copy_stream
+            with torch.cuda.stream(s):
+                for _ in range(2):
+                    dst.copy_(src, non_blocking=True)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(s)
+                for _ in range(16):
+                    dst.copy_(src, non_blocking=True)
+                e1.record(s)
+            e1.synchronize()
+            self._link_peak = 16 * src.numel() / (e0.elapsed_time(e1) / 1e3) / 1e9
+            self.cache.used[0] = False
+        return self._link_peak
+
+    def prefill_bytes_floor(self) -> int:
+        """sum_l |A_l| * expert bytes of the last prefill."""
+        n = sum(len(r["activated"]) for r in self.log if r["phase"] == "prefill")
+        return n * self.store.blob_bytes
+
+    def decode_bytes_floor(self) -> int:
+        """L * k * expert bytes per token (perfect prediction)."""
+        return self.L * self.k * self.store.blob_bytes
+
+    def hit_summary(self) -> dict:
+        dec = [r for r in self.log if r["phase"] == "decode" and "pred" in r]
+        hits = sum(len(set(r["pred"]) & set(r["gate"])) for r in dec)
+        miss = sum(len(r["refetch"]) for r in dec)
+        exact = sum(r["pred"] == r["gate"] for r in dec)
+        n = len(dec)
+        return {"policy": self.policy.value, "prefetch_hits": hits, "prefetch_misses": miss,
+                "topk_hit_rate": round(exact / n, 4) if n else None,
+                "at_least_one_rate": round(sum(bool(set(r["pred"]) & set(r["gate"])) for r in dec) / n, 4)
+                if n else None}
+
     def resident_bytes(self) -> dict:
         pred = self.driver.nbytes if isinstance(self.driver, MLPDriver) else 0
         return {"non_moe": self.W.nbytes(), "expert_slots": self.cache.nbytes, "predictor": pred,
                 "kv_cache": self.kv.nbytes, "model_total": self.shape.total_bytes}
+
+
+class KernelProfiler:
+    """CUDA-event spans around hot-path launches, on the launching stream.
+
+    Used by bench.py for the live roofline: algorithmic bytes / FLOPs per
+    launch divided by the event-measured duration."""
+
+    def __init__(self):
+        self.spans = {}          # name -> list of (ev0, ev1, bytes, flops)
+        self.launch0 = ops.launch_total()
+
+    def reset(self):
+        self.spans = {}
+        self.launch0 = ops.launch_total()
+
+    def start(self):
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        return ev
+
+    def stop(self, name: str, ev0, nbytes: float, flops: float = 0.0):
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev1.record()
+        self.spans.setdefault(name, []).append((ev0, ev1, nbytes, flops))
+
+    def summary(self, peaks: dict) -> dict:
+        torch.cuda.synchronize()
+        hbm = float(peaks.get("hbm_gbs", 6650.0))
+        tf = float(peaks.get("bf16_tflops", 1590.0))
+        out = []
+        for name, sp in self.spans.items():
+            t = sum(a.elapsed_time(b) for a, b, _, _ in sp) / 1e3
+            nb = sum(x[2] for x in sp)
+            fl = sum(x[3] for x in sp)
+            if fl > 0:
+                ach = fl / t / 1e12
+                out.append({"kernel": name, "bound": "tensor", "achieved": round(ach, 1), "peak": tf,
+                            "unit": "TFLOP/s", "frac": round(ach / tf, 4), "traffic": None,
+                            "launches": len(sp), "avg_us": round(1e6 * t / len(sp), 2),
+                            "total_ms": round(1e3 * t, 2), "bytes_per_launch": nb / len(sp),
+                            "flops_per_launch": fl / len(sp)})
+            else:
+                ach = nb / t / 1e9
+                out.append({"kernel": name, "bound": "hbm", "achieved": round(ach, 1), "peak": hbm,
+                            "unit": "GB/s", "frac": round(ach / hbm, 4), "traffic": None,
+                            "launches": len(sp), "avg_us": round(1e6 * t / len(sp), 2),
+                            "total_ms": round(1e3 * t, 2), "bytes_per_launch": nb / len(sp)})
+        out.sort(key=lambda r: -r["total_ms"])
+        dom = dict(out[0]) if out else None
+        return {"dominant": dom, "all": out, "launches": ops.launch_total() - self.launch0}

@@ -11,6 +11,18 @@ import torch
 from . import _lib
 from ._lib import ptr, stream_ptr
 
+# kernels launched by this process through the wrappers below (bench.py's
+# "gpu_launches" evidence); keyed by C-ABI entry point
+LAUNCHES: dict = {}
+
+
+def _count(name: str, n: int = 1) -> None:
+    LAUNCHES[name] = LAUNCHES.get(name, 0) + n
+
+
+def launch_total() -> int:
+    return sum(LAUNCHES.values())
+
 
 @lru_cache(maxsize=None)
 def expert_layout(d: int, ff: int, G: int):
@@ -32,6 +44,7 @@ def expert_struct(base_ptr: int, d: int, ff: int, G: int) -> _lib.W4Expert:
 
 def w4_generate(seed: int, layer: int, expert: int, d: int, ff: int, G: int, blob: torch.Tensor) -> None:
     _lib.call("ds_w4_generate", seed, layer, expert, d, ff, G, ptr(blob), stream_ptr())
+    _count("ds_w4_generate", 9)
 
 
 def gate_topk(x: torch.Tensor, wg: torch.Tensor, k: int, idx: torch.Tensor, w: torch.Tensor,
@@ -42,32 +55,38 @@ def gate_topk(x: torch.Tensor, wg: torch.Tensor, k: int, idx: torch.Tensor, w: t
     stride = hist.shape[-1] if hist is not None else 0
     _lib.call("ds_gate_topk", ptr(x), ptr(wg), T, d, M, k, ptr(idx), ptr(w), ptr(logits), ptr(counts),
               ptr(hist), stride, layer, stream_ptr())
+    _count("ds_gate_topk")
 
 
 def permute(idx: torch.Tensor, x: torch.Tensor, M: int, offsets, pos, src, xperm) -> None:
     T, k = idx.shape
     _lib.call("ds_permute", ptr(idx), ptr(x), T, x.shape[1], M, k, ptr(offsets), ptr(pos), ptr(src),
               ptr(xperm), stream_ptr())
+    _count("ds_permute", 2 if xperm is not None else 1)
 
 
 def unpermute_combine(y: torch.Tensor, pos, w, resid, out) -> None:
     T, k = w.shape
     _lib.call("ds_unpermute_combine", ptr(y), ptr(pos), ptr(w), ptr(resid), T, resid.shape[1], k, ptr(out),
               stream_ptr())
+    _count("ds_unpermute_combine")
 
 
 def swiglu_gemv(x: torch.Tensor, e: _lib.W4Expert, d: int, ff: int, G: int, h: torch.Tensor) -> None:
     _lib.call("ds_w4_swiglu_gemv", ptr(x), x.shape[0], C.byref(e), d, ff, G, ptr(h), stream_ptr())
+    _count("ds_w4_swiglu_gemv", (x.shape[0] + 3) // 4)
 
 
 def down_gemv(h: torch.Tensor, e: _lib.W4Expert, d: int, ff: int, G: int, route_w: torch.Tensor,
               route_stride: int, acc: torch.Tensor) -> None:
     _lib.call("ds_w4_down_gemv", ptr(h), h.shape[0], C.byref(e), d, ff, G, ptr(route_w), route_stride, ptr(acc),
               stream_ptr())
+    _count("ds_w4_down_gemv", (h.shape[0] + 3) // 4)
 
 
 def combine_finalize(acc: torch.Tensor, resid: torch.Tensor, out: torch.Tensor) -> None:
     _lib.call("ds_combine_finalize", ptr(acc), ptr(resid), resid.shape[0], resid.shape[1], ptr(out), stream_ptr())
+    _count("ds_combine_finalize")
 
 
 def grouped_ffn_workspace(rows: int, d: int, ff: int) -> int:
@@ -81,8 +100,10 @@ def grouped_ffn(xperm: torch.Tensor, offsets: list, experts: list, d: int, ff: i
     arr = (_lib.W4Expert * E)(*experts)
     _lib.call("ds_w4_grouped_ffn", ptr(xperm), off, E, arr, d, ff, G, ptr(h), ptr(y), ptr(ws), ws.numel(),
               stream_ptr())
+    _count("ds_w4_grouped_ffn", 3)
 
 
 def route_histogram(paths: torch.Tensor, M: int, pop_counts: torch.Tensor, aff_counts: torch.Tensor) -> None:
     N, L, k = paths.shape
     _lib.call("ds_route_histogram", ptr(paths), N, L, M, k, ptr(pop_counts), ptr(aff_counts), stream_ptr())
+    _count("ds_route_histogram")

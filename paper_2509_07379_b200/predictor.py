@@ -227,6 +227,8 @@ class DeviceMLP:
         if out is None:
             out = t.empty((B, topk), dtype=t.int32, device=self.device)
         ws = self.workspace(B)
+        from .ops import _count
+        _count("ds_predictor_forward", 1 if B <= 8 else 9)
         self.lib.call("ds_predictor_forward", self.desc, self.lib.ptr(self.packed), self.lib.ptr(hist),
                       self.lib.ptr(target), self.lib.ptr(pop_d), self.lib.ptr(aff_d), L, M, k, mode, B,
                       topk, self.lib.ptr(out), self.lib.ptr(probs), self.lib.ptr(ws), ws.numel(),
