@@ -260,6 +260,7 @@ def run_ours(args):
                      oracle_paths=paths, max_seq=args.prefill + args.decode + 8, max_prefill=args.prefill)
     setup_s = time.time() - t_setup
     prof = eng.enable_profile()
+    eng.link_peak_gbs()
 
     def one_step(n_decode: int):
         eng.reset()
@@ -288,6 +289,7 @@ def run_ours(args):
     for _ in range(args.warmup):
         one_step(wd)
     prof.reset()
+    torch.cuda.reset_peak_memory_stats(dev)     # residency = peak of the serving loop, not of setup
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
