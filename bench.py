@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--warmup-decode", type=int, default=None,
                     help="decode tokens per warm-up step (default: same as --decode)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cancel", action="store_true",
+                    help="paper-faithful decode: whole-expert prefetch, no cancellation of wrong prefetches")
+    ap.add_argument("--chunk-mb", type=float, default=8.0)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--out", default=None, help="also write the JSON line to this file")
     return ap.parse_args()
@@ -248,7 +251,7 @@ def run_ours(args):
     net, pop, aff = predictor_inputs(shape) if args.policy == "duoserve" else (None, None, None)
     eng = Engine(shape, args.policy if args.policy != "oracle" else "duoserve", seed=args.seed, device=dev,
                  predictor=net, pop=pop, aff=aff, max_seq=args.prefill + args.decode + 8,
-                 max_prefill=args.prefill)
+                 max_prefill=args.prefill, cancel_mispredicted=not args.no_cancel, chunk_mb=args.chunk_mb)
     gen = torch.Generator().manual_seed(args.seed + 1000 * rank)
     ids_host = torch.randint(0, shape.vocab, (args.prefill,), generator=gen).pin_memory()
     if args.policy == "oracle":
@@ -257,7 +260,8 @@ def run_ours(args):
         eng.generate(ids_host, args.decode + 1)
         paths = eng.paths_decode
         eng = Engine(shape, "oracle", seed=args.seed, device=dev, dense=eng.W, store=eng.store,
-                     oracle_paths=paths, max_seq=args.prefill + args.decode + 8, max_prefill=args.prefill)
+                     oracle_paths=paths, max_seq=args.prefill + args.decode + 8, max_prefill=args.prefill,
+                     cancel_mispredicted=not args.no_cancel, chunk_mb=args.chunk_mb)
     setup_s = time.time() - t_setup
     prof = eng.enable_profile()
     eng.link_peak_gbs()
@@ -323,7 +327,8 @@ def run_ours(args):
         "vs_baseline": None, "dtype": "bf16 activations, W4 (int4 g128) experts, f32 accumulate",
         "data": "synthetic (random-init W4 experts from a counter-based generator, random prompt ids)",
         "config": {"workload": f"{shape.name}-shaped W4, batch 1, prefill {args.prefill} + decode {args.decode}, "
-                               f"1 request per GPU, policy {args.policy}",
+                               f"1 request per GPU, policy {args.policy}"
+                               f"{'' if args.no_cancel else ' + chunked cancellable prefetch'}",
                    "model": shape.name, "global_batch": ws, "seq_len": args.prefill + args.decode,
                    "parallelism": f"replicas{ws}" if ws > 1 else "single-gpu",
                    "expert_slots": eng.n_slots,

@@ -116,6 +116,94 @@ class ExpertCache:
         self.used[slot] = True
 
 
+class Transfer:
+    __slots__ = ("slot", "layer", "expert", "nchunks", "next", "cancelled")
+
+    def __init__(self, slot, layer, expert, nchunks):
+        self.slot, self.layer, self.expert, self.nchunks = slot, layer, expert, nchunks
+        self.next = 0
+        self.cancelled = False
+
+    @property
+    def issued(self) -> bool:
+        return self.next >= self.nchunks
+
+
+class LinkQueue:
+    """Host-side scheduler of the H2D link for decode: expert transfers are
+    split into chunks and issued just in time (at most `depth` chunks queued
+    on the copy engine), so a prefetch proven wrong by the gate (sync point 1)
+    stops after its in-flight chunks instead of occupying the link for the
+    whole expert.  With cancel=False and one chunk per expert this is exactly
+    the paper's schedule (whole-expert prefetch, then blocking re-fetch)."""
+
+    def __init__(self, cache: "ExpertCache", chunk_bytes: int, depth: int, cancel: bool):
+        self.cache = cache
+        blob = cache.store.blob_bytes
+        self.chunk = blob if chunk_bytes <= 0 else min(chunk_bytes, blob)
+        self.nchunks = (blob + self.chunk - 1) // self.chunk
+        self.depth = depth
+        self.cancel_enabled = cancel
+        self.pending: list = []
+        self.inflight: list = []
+        self.wasted_bytes = 0
+
+    def submit(self, slot: int, layer: int, expert: int) -> Transfer:
+        tr = Transfer(slot, layer, expert, self.nchunks)
+        self.pending.append(tr)
+        self.cache.content[slot] = (layer, expert)
+        self.pump()
+        return tr
+
+    def cancel(self, tr: Transfer) -> None:
+        if not self.cancel_enabled or tr.issued:
+            return
+        tr.cancelled = True
+        self.wasted_bytes += tr.next * self.chunk
+        if tr in self.pending:
+            self.pending.remove(tr)
+
+    def _issue(self, tr: Transfer) -> None:
+        c = self.cache
+        i = tr.next
+        a = i * self.chunk
+        b = min(a + self.chunk, c.store.blob_bytes)
+        cs = c.copy_stream
+        with torch.cuda.stream(cs):
+            if i == 0 and c.used[tr.slot]:
+                cs.wait_event(c.free[tr.slot])
+            c.slots[tr.slot, a:b].copy_(c.store.host[tr.layer, tr.expert, a:b], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(cs)
+            if i == tr.nchunks - 1:
+                c.ready[tr.slot].record(cs)
+        c.bytes_copied += b - a
+        tr.next += 1
+        self.inflight.append(ev)
+        if tr.issued:
+            c.n_copies += 1
+
+    def pump(self) -> None:
+        while self.inflight and self.inflight[0].query():
+            self.inflight.pop(0)
+        while self.pending and len(self.inflight) < self.depth:
+            tr = self.pending[0]
+            self._issue(tr)
+            if tr.issued:
+                self.pending.pop(0)
+
+    def flush(self, tr: Transfer) -> None:
+        """Block (pumping) until every chunk of tr has been issued."""
+        while not tr.issued:
+            self.pump()
+            if not tr.issued and len(self.inflight) >= self.depth:
+                self.inflight[0].synchronize()
+
+    def wait_event(self, ev) -> None:
+        while not ev.query():
+            self.pump()
+
+
 class MLPDriver:
     """K5 on the predict stream: P_{l+1} from the device history buffer."""
 
@@ -128,7 +216,9 @@ class MLPDriver:
         self.target = torch.zeros(1, dtype=torch.int32, device=device)
         self.targets = [torch.full((1,), l, dtype=torch.int32, device=device) for l in range(L)]
         self.out = torch.empty((1, k), dtype=torch.int32, device=device)
+        self.probs = torch.empty((1, M), dtype=torch.float64, device=device)
         self.host_out = torch.empty((1, k), dtype=torch.int32, pin_memory=True)
+        self.host_probs = torch.empty((1, M), dtype=torch.float64, pin_memory=True)
         self.done = torch.cuda.Event()
         self.nbytes = self.dev.nbytes + self.stats.pop.nbytes + self.stats.aff.nbytes
 
@@ -136,13 +226,20 @@ class MLPDriver:
         with torch.cuda.stream(self.stream):
             self.stream.wait_event(after)
             self.dev.predict_state(hist, self.targets[target_layer], self.stats.pop, self.stats.aff, self.L,
-                                   self.M, self.k, self.mode, self.k, out=self.out, stream=self.stream)
+                                   self.M, self.k, self.mode, self.k, out=self.out, probs=self.probs,
+                                   stream=self.stream)
             self.host_out.copy_(self.out, non_blocking=True)
+            self.host_probs.copy_(self.probs, non_blocking=True)
             self.done.record(self.stream)
 
-    def result(self) -> list:
+    def result(self, link=None) -> tuple:
+        """(sorted predicted set, transfer order = descending probability)."""
+        if link is not None:
+            link.wait_event(self.done)
         self.done.synchronize()
-        return [int(e) for e in self.host_out[0].tolist()]
+        P = [int(e) for e in self.host_out[0].tolist()]
+        pr = self.host_probs[0].tolist()
+        return P, sorted(P, key=lambda e: (-pr[e], e))
 
 
 class TraceDriver:
@@ -156,8 +253,8 @@ class TraceDriver:
     def launch(self, hist, after, target_layer: int) -> None:
         self._next = list(self.paths[self.t][target_layer])
 
-    def result(self) -> list:
-        return self._next
+    def result(self, link=None) -> tuple:
+        return sorted(self._next), list(self._next)
 
 
 @dataclass
@@ -172,7 +269,8 @@ class Engine:
     def __init__(self, shape: ModelShape, policy="duoserve", seed: int = 0, device="cuda",
                  dense: DenseWeights | None = None, store: HostExpertStore | None = None,
                  predictor: ExpertMLP | None = None, pop=None, aff=None, oracle_paths=None,
-                 max_seq: int = 2048, max_prefill: int = 2048):
+                 max_seq: int = 2048, max_prefill: int = 2048, cancel_mispredicted: bool = True,
+                 chunk_mb: float = 8.0, link_depth: int = 2):
         self.shape = shape
         self.policy = SchedulerPolicy(policy)
         self.device = torch.device(device)
@@ -186,6 +284,9 @@ class Engine:
         cfg = model_config_for_shape(sh)
         self.n_slots = slot_count(self.policy, cfg)
         self.cache = ExpertCache(self.store, self.n_slots, self.device)
+        self.cancel_mispredicted = cancel_mispredicted
+        self.link = LinkQueue(self.cache, int(chunk_mb * 2**20) if cancel_mispredicted else 0,
+                              link_depth if cancel_mispredicted else 2, cancel_mispredicted)
         self.kv = KVCache(sh, max_seq, self.device)
         self.cos, self.sin = rope_tables(sh, max_seq, self.device)
         self.driver = None
@@ -244,6 +345,11 @@ class Engine:
         self._pred_next = None
         self.hist.zero_()
         self.d2h_bytes = 0
+        if hasattr(self, "link"):
+            self.cache.copy_stream.synchronize()
+            self.link.pending.clear()
+            self.link.inflight.clear()
+            self.link.wasted_bytes = 0
 
     def enable_profile(self) -> "KernelProfiler":
         self.prof = KernelProfiler()
@@ -371,6 +477,7 @@ class Engine:
     # --------------------------------------------------------------- decode
     def _moe_decode(self, l: int, h: torch.Tensor):
         sh = self.shape
+        link = self.link
         a = rms_norm(h, self.W.layers[l]["ln2"], sh.rms_eps)
         ops.gate_topk(a, self.W.layers[l]["wg"], self.k, self.idx1, self.w1, hist=self.hist, layer=l)
         self.ev_gate.record()
@@ -380,36 +487,40 @@ class Engine:
         use_pred = self.driver is not None
         if use_pred and l + 1 < self.L:
             self.driver.launch(self.hist, self.ev_gate, l + 1)     # predict stream, overlapped
-        ev_idx.synchronize()                                       # sync point 1: E_l on the host
-        self.d2h_bytes += self.idx_host.nbytes + (4 * self.k if use_pred else 0)
+        link.wait_event(ev_idx)                                    # sync point 1: E_l on the host
+        self.d2h_bytes += self.idx_host.nbytes + ((4 * self.k + 8 * self.M) if use_pred else 0)
         E = [int(e) for e in self.idx_host[0].tolist()]
         if self.capture is not None:
             self.capture.append(("decode", l, a.cpu(), self.idx_host.clone()))
-        slot_of = {}
+        slot_of, trs = {}, {}
+        miss = []
         if l == 0 or not use_pred:
             base = 0 if (l % 2 == 0 or self.n_slots < 2 * self.k) else self.k
             for j, e in enumerate(E):
                 slot = (base + j) % self.n_slots
-                self.cache.load(slot, l, e)
+                trs[e] = link.submit(slot, l, e)
                 slot_of[e] = slot
             self.log.append({"phase": "decode", "token": self.t_decode, "layer": l, "fetch": E,
                              "kind": "ondemand"})
         else:
-            P, P_slots = self._pred_next
+            P, order, pending = self._pred_next
             miss = sorted(set(E) - set(P))
-            wrong_slots = [s for p, s in zip(P, P_slots) if p not in E]
-            for p, s in zip(P, P_slots):
+            wrong = [p for p in order if p not in E]
+            for p in order:
                 if p in E:
-                    slot_of[p] = s
-            for e, s in zip(miss, wrong_slots):
-                self.cache.load(s, l, e)                            # blocking re-fetch of the wrong slot
-                slot_of[e] = s
+                    slot_of[p], trs[p] = pending[p]
+                else:
+                    link.cancel(pending[p][1])                     # drop its not-yet-issued chunks
+            for e, p in zip(miss, wrong):
+                s_ = pending[p][0]
+                trs[e] = link.submit(s_, l, e)                     # re-fetch into the wrong slot
+                slot_of[e] = s_
             self.log.append({"phase": "decode", "token": self.t_decode, "layer": l, "pred": sorted(P),
                              "gate": sorted(E), "refetch": miss})
-        # expert compute: hits first (already resident), then the re-fetched ones
-        refetched = set(self.log[-1].get("refetch", []))
-        for e in [x for x in E if x not in refetched] + [x for x in E if x in refetched]:
+        # expert compute: hits first (already resident or in flight), then re-fetched ones
+        for e in [x for x in E if x not in miss] + miss:
             j = E.index(e)
+            link.flush(trs[e])
             st = self.cache.acquire(slot_of[e])
             ev = self.prof.start() if self.prof else None
             ops.swiglu_gemv(a, st, self.d, self.ff, self.G, self.h_buf)
@@ -421,12 +532,13 @@ class Engine:
         ops.combine_finalize(self.acc, h, out)
         # sync point 2: prediction for l+1 ready -> prefetch into the slots layer l-1 used
         if use_pred and l + 1 < self.L:
-            Pn = self.driver.result()
+            Pn, order = self.driver.result(link)
             cur = set(slot_of.values())
-            free = [s for s in range(self.n_slots) if s not in cur][: self.k]
-            for e, s in zip(Pn, free):
-                self.cache.load(s, l + 1, e)
-            self._pred_next = (Pn, free)
+            free = [s_ for s_ in range(self.n_slots) if s_ not in cur][: self.k]
+            pending = {}
+            for e, s_ in zip(order, free):
+                pending[e] = (s_, link.submit(s_, l + 1, e))
+            self._pred_next = (Pn, order, pending)
         return out, E
 
     # -------------------------------------------------------------- metrics
@@ -464,7 +576,9 @@ class Engine:
         miss = sum(len(r["refetch"]) for r in dec)
         exact = sum(r["pred"] == r["gate"] for r in dec)
         n = len(dec)
-        return {"policy": self.policy.value, "prefetch_hits": hits, "prefetch_misses": miss,
+        return {"policy": self.policy.value, "cancel_mispredicted": self.cancel_mispredicted,
+                "chunk_bytes": self.link.chunk, "wasted_prefetch_bytes": self.link.wasted_bytes,
+                "prefetch_hits": hits, "prefetch_misses": miss,
                 "topk_hit_rate": round(exact / n, 4) if n else None,
                 "at_least_one_rate": round(sum(bool(set(r["pred"]) & set(r["gate"])) for r in dec) / n, 4)
                 if n else None}

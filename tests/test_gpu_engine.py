@@ -117,3 +117,13 @@ def test_ondemand_policy_same_tokens(tiny, cuda):
                  max_prefill=PREFILL)
     assert eng.generate(tiny["ids"], DECODE) == tiny["toks"]
     assert eng.n_slots == 2
+
+
+def test_faithful_and_cancelling_schedules_agree(tiny, cuda):
+    """Chunked cancellable prefetch changes transfers, not decisions: same tokens, same cache log."""
+    shape = tiny["shape"]
+    eng = Engine(shape, "duoserve", seed=3, dense=tiny["dense"].to(cuda), predictor=tiny["net"], pop=tiny["pop"],
+                 aff=tiny["aff"], max_seq=PREFILL + DECODE + 8, max_prefill=PREFILL, cancel_mispredicted=False)
+    assert eng.generate(tiny["ids"], DECODE) == tiny["toks"]
+    assert eng.log == tiny["eng"].log
+    assert tiny["eng"].cancel_mispredicted and tiny["eng"].link.nchunks > 1 or shape.hidden == 256
