@@ -113,119 +113,126 @@ __device__ __forceinline__ void stage_x(const __nv_bfloat16* __restrict__ x, int
     __syncthreads();
 }
 
-// Partial dot of one lane's 32 codes against its x chunk: sum x*(128+q).
-// xc = start of the (swizzled) chunk, sw = (chunk >> 1) & 3.
-__device__ __forceinline__ float dot32(const uint4 c, const uint32_t* xc, int sw) {
-    float acc = 0.f;
-    const uint32_t cw[4] = {c.x, c.y, c.z, c.w};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const uint4 xv = *reinterpret_cast<const uint4*>(xc + 4 * (i ^ sw));
-        const uint32_t xx[4] = {xv.x, xv.y, xv.z, xv.w};
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {
-            const uint32_t p = nib_pair_magic(cw[i] >> (4 * s));
-            fma_bf16_lo(acc, p, xx[s]);
-            fma_bf16_hi(acc, p, xx[s]);
-        }
-    }
-    return acc;
-}
-
-__device__ __forceinline__ float group_term(const W4Ptr& m, int n, int gpr, int g, float part,
-                                            float xsum) {
-    const size_t zi = (size_t)n * gpr + g;
-    const float z = (float)((__ldg(m.zeros + (zi >> 1)) >> ((zi & 1) * 4)) & 15);
-    const float s = __uint_as_float((uint32_t)__ldg(m.scales + zi) << 16);
-    return s * (part - (128.f + z) * xsum);
-}
-
-// h[r, n] = bf16( silu(x_r . W1[:, n]) * (x_r . W3[:, n]) )
-__global__ void __launch_bounds__(kGemvThreads) swiglu_gemv_kernel(
-    const __nv_bfloat16* __restrict__ x, int R, W4Ptr w1, W4Ptr w3, int K, int N, int G,
-    __nv_bfloat16* __restrict__ h) {
-    extern __shared__ __align__(16) uint32_t sm[];
-    uint32_t* xs = sm;                               // R * K/2 words
-    float* xsum = reinterpret_cast<float*>(sm + R * K / 2);  // R * K/32
-    stage_x(x, R, K, xs, xsum);
+// One warp per output row n (NMAT = 2: rows n of W1 and W3 for SwiGLU;
+// NMAT = 1: row n of W2).  Lane l owns the 32-code chunks c = l + 32 i; the
+// loads for U chunks x NMAT matrices (codes, scale, zero) are issued back to
+// back before any math so each warp keeps U*NMAT*16 B per lane in flight.
+template <int R, int NMAT, int U>
+__device__ __forceinline__ void gemv_row(const W4Ptr (&W)[NMAT], int n, int K, int G,
+                                         const uint32_t* __restrict__ xs, const float* __restrict__ xsum,
+                                         float (&acc)[NMAT][R]) {
     const int lane = threadIdx.x & 31;
-    const int warps = gridDim.x * (blockDim.x >> 5);
+    const int nchunks = K / 32;
     const int gpr = K / G;
-    const int kwords = K / 8;
-    for (int n = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); n < N; n += warps) {
-        float a[kRMax], b[kRMax];
+    const int cpg = G / 32;                     // chunks per group
+    const size_t row_w = (size_t)K / 8;         // words per row
 #pragma unroll
-        for (int r = 0; r < kRMax; ++r) a[r] = b[r] = 0.f;
-        const uint4* c1 = reinterpret_cast<const uint4*>(w1.codes + (size_t)n * kwords);
-        const uint4* c3 = reinterpret_cast<const uint4*>(w3.codes + (size_t)n * kwords);
-#pragma unroll 2
-        for (int kk = lane * 32; kk < K; kk += 1024) {
-            const uint4 v1 = ldg_nc_v4(c1 + (kk >> 5));
-            const uint4 v3 = ldg_nc_v4(c3 + (kk >> 5));
-            const int g = kk / G;
+    for (int m = 0; m < NMAT; ++m)
 #pragma unroll
-            for (int r = 0; r < kRMax; ++r) {
-                if (r < R) {
-                    const uint32_t* xc = xs + (size_t)r * (K / 2) + kk / 2;
-                    const int sw = (kk >> 6) & 3;
-                    const float xsm = xsum[r * (K / 32) + (kk >> 5)];
-                    a[r] += group_term(w1, n, gpr, g, dot32(v1, xc, sw), xsm);
-                    b[r] += group_term(w3, n, gpr, g, dot32(v3, xc, sw), xsm);
+        for (int r = 0; r < R; ++r) acc[m][r] = 0.f;
+    for (int c0 = lane; c0 < nchunks; c0 += 32 * U) {
+        uint4 cv[U][NMAT];
+        uint16_t sv[U][NMAT];
+        uint8_t zv[U][NMAT];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int c = c0 + 32 * u;
+            if (c < nchunks) {
+                const size_t gi = (size_t)n * gpr + c / cpg;
+#pragma unroll
+                for (int m = 0; m < NMAT; ++m) {
+                    cv[u][m] = ldg_nc_v4(W[m].codes + (size_t)n * row_w + (size_t)c * 4);
+                    sv[u][m] = __ldg(W[m].scales + gi);
+                    zv[u][m] = __ldg(W[m].zeros + (gi >> 1));
                 }
             }
         }
 #pragma unroll
-        for (int r = 0; r < kRMax; ++r) {
-            if (r < R) {
-                const float av = warp_sum(a[r]);
-                const float bv = warp_sum(b[r]);
-                if (lane == r) {
-                    const float sl = av / (1.0f + expf(-av));
-                    h[(size_t)r * N + n] = __float2bfloat16_rn(sl * bv);
+        for (int u = 0; u < U; ++u) {
+            const int c = c0 + 32 * u;
+            if (c < nchunks) {
+                const size_t gi = (size_t)n * gpr + c / cpg;
+                const int sw = (c >> 1) & 3;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const uint32_t* xc = xs + (size_t)r * (K / 2) + c * 16;
+                    const float xsm = xsum[r * nchunks + c];
+                    uint4 xv[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) xv[i] = *reinterpret_cast<const uint4*>(xc + 4 * (i ^ sw));
+#pragma unroll
+                    for (int m = 0; m < NMAT; ++m) {
+                        const uint32_t cw[4] = {cv[u][m].x, cv[u][m].y, cv[u][m].z, cv[u][m].w};
+                        float p0 = 0.f, p1 = 0.f;
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const uint32_t xx[4] = {xv[i].x, xv[i].y, xv[i].z, xv[i].w};
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                const uint32_t pr = nib_pair_magic(cw[i] >> (4 * q));
+                                fma_bf16_lo(p0, pr, xx[q]);
+                                fma_bf16_hi(p1, pr, xx[q]);
+                            }
+                        }
+                        const float z = (float)((zv[u][m] >> ((gi & 1) * 4)) & 15);
+                        const float sc = __uint_as_float((uint32_t)sv[u][m] << 16);
+                        acc[m][r] = fmaf(sc, (p0 + p1) - (128.f + z) * xsm, acc[m][r]);
+                    }
                 }
+            }
+        }
+    }
+#pragma unroll
+    for (int m = 0; m < NMAT; ++m)
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[m][r] = warp_sum(acc[m][r]);
+}
+
+// h[r, n] = bf16( silu(x_r . W1[:, n]) * (x_r . W3[:, n]) )
+template <int R>
+__global__ void __launch_bounds__(kGemvThreads) swiglu_gemv_kernel(
+    const __nv_bfloat16* __restrict__ x, W4Ptr w1, W4Ptr w3, int K, int N, int G,
+    __nv_bfloat16* __restrict__ h) {
+    extern __shared__ __align__(16) uint32_t sm[];
+    uint32_t* xs = sm;
+    float* xsum = reinterpret_cast<float*>(sm + R * K / 2);
+    stage_x(x, R, K, xs, xsum);
+    const int lane = threadIdx.x & 31;
+    const int warps = gridDim.x * (blockDim.x >> 5);
+    const W4Ptr W[2] = {w1, w3};
+    for (int n = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); n < N; n += warps) {
+        float acc[2][R];
+        gemv_row<R, 2, 2>(W, n, K, G, xs, xsum, acc);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            if (lane == r) {
+                const float av = acc[0][r], bv = acc[1][r];
+                h[(size_t)r * N + n] = __float2bfloat16_rn(av / (1.0f + expf(-av)) * bv);
             }
         }
     }
 }
 
 // acc[r, n] += route_w[r] * (h_r . W2[:, n])
+template <int R>
 __global__ void __launch_bounds__(kGemvThreads) down_gemv_kernel(
-    const __nv_bfloat16* __restrict__ hin, int R, W4Ptr w2, int K, int N, int G,
-    const float* __restrict__ route_w, int route_stride, float* __restrict__ acc) {
+    const __nv_bfloat16* __restrict__ hin, W4Ptr w2, int K, int N, int G, const float* __restrict__ route_w,
+    int route_stride, float* __restrict__ out) {
     extern __shared__ __align__(16) uint32_t sm[];
     uint32_t* xs = sm;
     float* xsum = reinterpret_cast<float*>(sm + R * K / 2);
     stage_x(hin, R, K, xs, xsum);
     const int lane = threadIdx.x & 31;
     const int warps = gridDim.x * (blockDim.x >> 5);
-    const int gpr = K / G;
-    const int kwords = K / 8;
+    const W4Ptr W[1] = {w2};
     for (int n = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); n < N; n += warps) {
-        float y[kRMax];
+        float acc[1][R];
+        gemv_row<R, 1, 4>(W, n, K, G, xs, xsum, acc);
 #pragma unroll
-        for (int r = 0; r < kRMax; ++r) y[r] = 0.f;
-        const uint4* c2 = reinterpret_cast<const uint4*>(w2.codes + (size_t)n * kwords);
-#pragma unroll 4
-        for (int kk = lane * 32; kk < K; kk += 1024) {
-            const uint4 v = ldg_nc_v4(c2 + (kk >> 5));
-            const int g = kk / G;
-#pragma unroll
-            for (int r = 0; r < kRMax; ++r) {
-                if (r < R) {
-                    const uint32_t* xc = xs + (size_t)r * (K / 2) + kk / 2;
-                    y[r] += group_term(w2, n, gpr, g, dot32(v, xc, (kk >> 6) & 3),
-                                       xsum[r * (K / 32) + (kk >> 5)]);
-                }
-            }
-        }
-#pragma unroll
-        for (int r = 0; r < kRMax; ++r) {
-            if (r < R) {
-                const float yv = warp_sum(y[r]);
-                if (lane == r) {
-                    float* o = acc + (size_t)r * N + n;
-                    *o = __fadd_rn(*o, __fmul_rn(route_w[(size_t)r * route_stride], yv));
-                }
+        for (int r = 0; r < R; ++r) {
+            if (lane == r) {
+                float* o = out + (size_t)r * N + n;
+                *o = __fadd_rn(*o, __fmul_rn(route_w[(size_t)r * route_stride], acc[0][r]));
             }
         }
     }
@@ -314,25 +321,50 @@ static int check_gemv_shape(int R, int d, int ff, int G) {
     return DS_OK;
 }
 
-extern "C" int ds_w4_swiglu_gemv(const void* x, int R, const ds_w4_expert* e, int d, int ff, int G,
-                                 void* h, void* stream) {
+template <int R>
+static int swiglu_launch(const __nv_bfloat16* x, const ds_w4_expert* e, int d, int ff, int G, __nv_bfloat16* h,
+                         cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(swiglu_gemv_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
+    const size_t smem = (size_t)R * d * 2 + (size_t)R * (d / 32) * 4;
+    const int grid = gemv_grid((const void*)swiglu_gemv_kernel<R>, smem, ff);
+    swiglu_gemv_kernel<R><<<grid, kGemvThreads, smem, st>>>(x, to_ptr(e->w1), to_ptr(e->w3), d, ff, G, h);
+    DS_LAUNCH_CHECK("ds_w4_swiglu_gemv");
+    return DS_OK;
+}
+
+template <int R>
+static int down_launch(const __nv_bfloat16* h, const ds_w4_expert* e, int d, int ff, int G, const float* rw,
+                       int rs, float* acc, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(down_gemv_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
+    const size_t smem = (size_t)R * ff * 2 + (size_t)R * (ff / 32) * 4;
+    const int grid = gemv_grid((const void*)down_gemv_kernel<R>, smem, d);
+    down_gemv_kernel<R><<<grid, kGemvThreads, smem, st>>>(h, to_ptr(e->w2), ff, d, G, rw, rs, acc);
+    DS_LAUNCH_CHECK("ds_w4_down_gemv");
+    return DS_OK;
+}
+
+extern "C" int ds_w4_swiglu_gemv(const void* x, int R, const ds_w4_expert* e, int d, int ff, int G, void* h,
+                                 void* stream) {
     int rc = check_gemv_shape(R, d, ff, G);
     if (rc) return rc;
     DS_CHECK_ARG(e && check_linear(e->w1) && check_linear(e->w3) && x && h, "ds_w4_swiglu_gemv: NULL pointer");
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(swiglu_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-        attr = true;
-    }
     cudaStream_t st = as_stream(stream);
-    for (int r0 = 0; r0 < R; r0 += kRMax) {
-        const int rr = R - r0 < kRMax ? R - r0 : kRMax;
-        const size_t smem = (size_t)rr * d * 2 + (size_t)rr * (d / 32) * 4;
-        const int grid = gemv_grid((const void*)swiglu_gemv_kernel, smem, ff);
-        swiglu_gemv_kernel<<<grid, kGemvThreads, smem, st>>>(
-            (const __nv_bfloat16*)x + (size_t)r0 * d, rr, to_ptr(e->w1), to_ptr(e->w3), d, ff, G,
-            (__nv_bfloat16*)h + (size_t)r0 * ff);
-        DS_LAUNCH_CHECK("ds_w4_swiglu_gemv");
+    const __nv_bfloat16* xb = (const __nv_bfloat16*)x;
+    __nv_bfloat16* hb = (__nv_bfloat16*)h;
+    for (int r0 = 0; r0 < R;) {
+        const int left = R - r0;
+        if (left >= 4) { rc = swiglu_launch<4>(xb + (size_t)r0 * d, e, d, ff, G, hb + (size_t)r0 * ff, st); r0 += 4; }
+        else if (left >= 2) { rc = swiglu_launch<2>(xb + (size_t)r0 * d, e, d, ff, G, hb + (size_t)r0 * ff, st); r0 += 2; }
+        else { rc = swiglu_launch<1>(xb + (size_t)r0 * d, e, d, ff, G, hb + (size_t)r0 * ff, st); r0 += 1; }
+        if (rc) return rc;
     }
     return DS_OK;
 }
@@ -342,20 +374,16 @@ extern "C" int ds_w4_down_gemv(const void* h, int R, const ds_w4_expert* e, int 
     int rc = check_gemv_shape(R, d, ff, G);
     if (rc) return rc;
     DS_CHECK_ARG(e && check_linear(e->w2) && h && route_w && acc, "ds_w4_down_gemv: NULL pointer");
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(down_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-        attr = true;
-    }
     cudaStream_t st = as_stream(stream);
-    for (int r0 = 0; r0 < R; r0 += kRMax) {
-        const int rr = R - r0 < kRMax ? R - r0 : kRMax;
-        const size_t smem = (size_t)rr * ff * 2 + (size_t)rr * (ff / 32) * 4;
-        const int grid = gemv_grid((const void*)down_gemv_kernel, smem, d);
-        down_gemv_kernel<<<grid, kGemvThreads, smem, st>>>(
-            (const __nv_bfloat16*)h + (size_t)r0 * ff, rr, to_ptr(e->w2), ff, d, G,
-            route_w + (size_t)r0 * route_stride, route_stride, acc + (size_t)r0 * d);
-        DS_LAUNCH_CHECK("ds_w4_down_gemv");
+    const __nv_bfloat16* hb = (const __nv_bfloat16*)h;
+    for (int r0 = 0; r0 < R;) {
+        const int left = R - r0;
+        const size_t ho = (size_t)r0 * ff, ao = (size_t)r0 * d;
+        const float* rw = route_w + (size_t)r0 * route_stride;
+        if (left >= 4) { rc = down_launch<4>(hb + ho, e, d, ff, G, rw, route_stride, acc + ao, st); r0 += 4; }
+        else if (left >= 2) { rc = down_launch<2>(hb + ho, e, d, ff, G, rw, route_stride, acc + ao, st); r0 += 2; }
+        else { rc = down_launch<1>(hb + ho, e, d, ff, G, rw, route_stride, acc + ao, st); r0 += 1; }
+        if (rc) return rc;
     }
     return DS_OK;
 }
