@@ -268,7 +268,7 @@ def run_ours(args):
 
     def one_step(n_decode: int):
         eng.reset()
-        c0 = eng.cache.bytes_copied
+        c0 = eng.h2d_bytes()
         s = torch.cuda.current_stream()
         e0, e1, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True), \
             torch.cuda.Event(enable_timing=True)
@@ -286,7 +286,7 @@ def run_ours(args):
         w2 = time.perf_counter()
         return {"ttft_ms": e0.elapsed_time(e1), "decode_ms": e1.elapsed_time(e2),
                 "e2e_wall_ms": 1e3 * (w2 - w0), "ttft_wall_ms": 1e3 * (w1 - w0),
-                "h2d_experts": eng.cache.bytes_copied - c0, "tokens": toks,
+                "h2d_experts": eng.h2d_bytes() - c0, "tokens": toks,
                 "d2h": eng.d2h_bytes}
 
     wd = args.warmup_decode if args.warmup_decode is not None else args.decode

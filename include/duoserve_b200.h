@@ -182,6 +182,27 @@ int ds_w4_grouped_ffn(const void *xperm, const int32_t *offsets, int E, const ds
                       int d, int ff, int G, void *h, float *y, void *workspace,
                       size_t workspace_bytes, void *stream);
 
+/* ========================================================================
+ * K6 — host->device expert link (copy engine), native scheduler thread.
+ * Replaces the paper's communication stream (SPEC's single
+ * serial link).  Transfers are issued in `chunk_bytes` pieces,
+ * at most `depth` queued on `copy_stream`; before the first chunk the stream
+ * waits `wait_event`, after the last `done_event` is recorded (both raw
+ * cudaEvent_t, may be NULL).  ds_link_cancel drops the chunks not yet issued
+ * (a prefetch proven wrong at sync point 1).
+ * ===================================================================== */
+typedef struct ds_link ds_link;
+int ds_link_create(void *copy_stream, size_t chunk_bytes, int depth, ds_link **out);
+int ds_link_destroy(ds_link *link);
+int ds_link_submit(ds_link *link, void *dst, const void *src, size_t bytes, void *wait_event,
+                   void *done_event, uint64_t *ticket);
+int ds_link_cancel(ds_link *link, uint64_t ticket, size_t *bytes_issued);
+/* Block until every chunk of `ticket` is issued (its done_event recorded) or it was cancelled. */
+int ds_link_wait_issued(ds_link *link, uint64_t ticket);
+int ds_link_idle(ds_link *link);
+int ds_link_stats(ds_link *link, uint64_t *bytes_issued, uint64_t *bytes_wasted, uint64_t *chunks);
+int ds_link_reset_stats(ds_link *link);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -80,6 +80,14 @@ _SIGS = {
     "ds_w4_down_gemv": (_I, [_P, _I, C.POINTER(W4Expert), _I, _I, _I, _P, _I, _P, _P]),
     "ds_combine_finalize": (_I, [_P, _P, _I, _I, _P, _P]),
     "ds_w4_grouped_ffn_workspace": (_SZ, [_I, _I, _I]),
+    "ds_link_create": (_I, [_P, _SZ, _I, C.POINTER(_P)]),
+    "ds_link_destroy": (_I, [_P]),
+    "ds_link_submit": (_I, [_P, _P, _P, _SZ, _P, _P, C.POINTER(C.c_uint64)]),
+    "ds_link_cancel": (_I, [_P, C.c_uint64, C.POINTER(_SZ)]),
+    "ds_link_wait_issued": (_I, [_P, C.c_uint64]),
+    "ds_link_idle": (_I, [_P]),
+    "ds_link_stats": (_I, [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "ds_link_reset_stats": (_I, [_P]),
     "ds_w4_grouped_ffn": (_I, [_P, C.POINTER(_I), _I, C.POINTER(W4Expert), _I, _I, _I, _P, _P, _P, _SZ, _P]),
 }
 

@@ -1,0 +1,228 @@
+// K6 — the host->device expert link: a native scheduler thread that feeds the
+// copy engine in chunks.
+//
+// experts stream from the pinned "CPU expert cache" to the
+// GPU expert cache on a dedicated communication stream.  The decode schedule
+// needs two things a plain cudaMemcpyAsync queue cannot give:
+//   * just-in-time issue — at most `depth` chunks are queued on the copy
+//     engine, so a prefetch that the gate proves wrong (sync point 1,
+//     PAPER.md:185) can be cancelled after its in-flight chunks instead of
+//     holding the link for the whole 91.5 MB expert;
+//   * continuity — the queue is topped up by this thread, not by the Python
+//     thread that is busy launching attention/gate kernels, so the link never
+//     drains while the host is launching work.
+// Per transfer: the copy stream first waits `wait_event` (the slot's last
+// compute), then the chunks are issued, then `done_event` is recorded (the
+// slot's ready event, waited on by the compute stream).
+#include "ds_common.cuh"
+
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <deque>
+#include <mutex>
+#include <thread>
+#include <memory>
+#include <unordered_map>
+#include <vector>
+
+namespace ds {
+namespace {
+
+struct Xfer {
+    uint64_t ticket;
+    char* dst;
+    const char* src;
+    size_t bytes;
+    size_t next = 0;        // bytes already issued
+    cudaEvent_t wait_ev;
+    cudaEvent_t done_ev;
+    bool cancelled = false;
+    bool issued = false;
+};
+
+}  // namespace
+}  // namespace ds
+
+struct ds_link {
+    cudaStream_t stream;
+    size_t chunk;
+    int depth;
+    int device;
+    std::mutex mu;
+    std::condition_variable cv;       // wakes the worker
+    std::condition_variable cv_done;  // wakes waiters
+    std::deque<std::shared_ptr<ds::Xfer>> pending;
+    std::unordered_map<uint64_t, std::shared_ptr<ds::Xfer>> live;
+    std::deque<cudaEvent_t> inflight;
+    std::vector<cudaEvent_t> pool;
+    uint64_t next_ticket = 1;
+    uint64_t bytes_issued = 0, bytes_wasted = 0, chunks = 0;
+    int error = 0;
+    bool stop = false;
+    std::thread worker;
+};
+
+namespace ds {
+namespace {
+
+cudaEvent_t take_event(ds_link* L) {
+    if (!L->pool.empty()) {
+        cudaEvent_t e = L->pool.back();
+        L->pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    return e;
+}
+
+// Issue as many chunks as the depth allows.  Called with L->mu held.
+void issue_locked(ds_link* L) {
+    while (!L->inflight.empty() && cudaEventQuery(L->inflight.front()) == cudaSuccess) {
+        L->pool.push_back(L->inflight.front());
+        L->inflight.pop_front();
+    }
+    while (!L->pending.empty() && (int)L->inflight.size() < L->depth) {
+        auto x = L->pending.front();
+        if (x->next == 0 && x->wait_ev) cudaStreamWaitEvent(L->stream, x->wait_ev, 0);
+        const size_t n = std::min(L->chunk, x->bytes - x->next);
+        cudaError_t e = cudaMemcpyAsync(x->dst + x->next, x->src + x->next, n, cudaMemcpyHostToDevice, L->stream);
+        if (e != cudaSuccess) L->error = (int)e;
+        cudaEvent_t ev = take_event(L);
+        cudaEventRecord(ev, L->stream);
+        L->inflight.push_back(ev);
+        x->next += n;
+        L->bytes_issued += n;
+        L->chunks++;
+        if (x->next >= x->bytes) {
+            if (x->done_ev) cudaEventRecord(x->done_ev, L->stream);
+            x->issued = true;
+            L->pending.pop_front();
+            L->live.erase(x->ticket);
+            L->cv_done.notify_all();
+        }
+    }
+}
+
+void worker_loop(ds_link* L) {
+    cudaSetDevice(L->device);
+    std::unique_lock<std::mutex> lk(L->mu);
+    while (!L->stop) {
+        issue_locked(L);
+        if (L->pending.empty()) {
+            L->cv.wait_for(lk, std::chrono::microseconds(200));
+        } else {
+            // queue full: poll the oldest chunk without holding the lock
+            lk.unlock();
+            std::this_thread::sleep_for(std::chrono::microseconds(4));
+            lk.lock();
+        }
+    }
+}
+
+}  // namespace
+}  // namespace ds
+
+using namespace ds;
+
+extern "C" int ds_link_create(void* copy_stream, size_t chunk_bytes, int depth, ds_link** out) {
+    DS_CHECK_ARG(out && chunk_bytes >= 4096 && depth >= 1 && depth <= 64, "ds_link_create: bad arguments");
+    ds_link* L = new ds_link();
+    L->stream = as_stream(copy_stream);
+    L->chunk = chunk_bytes;
+    L->depth = depth;
+    cudaGetDevice(&L->device);
+    L->worker = std::thread(worker_loop, L);
+    *out = L;
+    return DS_OK;
+}
+
+extern "C" int ds_link_destroy(ds_link* L) {
+    if (!L) return DS_OK;
+    {
+        std::lock_guard<std::mutex> g(L->mu);
+        L->stop = true;
+    }
+    L->cv.notify_all();
+    L->worker.join();
+    cudaStreamSynchronize(L->stream);
+    for (auto e : L->inflight) cudaEventDestroy(e);
+    for (auto e : L->pool) cudaEventDestroy(e);
+    delete L;
+    return DS_OK;
+}
+
+extern "C" int ds_link_submit(ds_link* L, void* dst, const void* src, size_t bytes, void* wait_event,
+                              void* done_event, uint64_t* ticket) {
+    DS_CHECK_ARG(L && dst && src && bytes > 0 && ticket, "ds_link_submit: bad arguments");
+    auto x = std::make_shared<Xfer>();
+    x->dst = static_cast<char*>(dst);
+    x->src = static_cast<const char*>(src);
+    x->bytes = bytes;
+    x->wait_ev = static_cast<cudaEvent_t>(wait_event);
+    x->done_ev = static_cast<cudaEvent_t>(done_event);
+    {
+        std::lock_guard<std::mutex> g(L->mu);
+        x->ticket = L->next_ticket++;
+        L->pending.push_back(x);
+        L->live[x->ticket] = x;
+        *ticket = x->ticket;
+        issue_locked(L);
+    }
+    L->cv.notify_one();
+    return DS_OK;
+}
+
+extern "C" int ds_link_cancel(ds_link* L, uint64_t ticket, size_t* bytes_issued) {
+    DS_CHECK_ARG(L, "ds_link_cancel: NULL link");
+    std::lock_guard<std::mutex> g(L->mu);
+    auto it = L->live.find(ticket);
+    size_t done = 0;
+    if (it != L->live.end()) {
+        auto x = it->second;
+        done = x->next;
+        x->cancelled = true;
+        L->bytes_wasted += x->next;
+        for (auto p = L->pending.begin(); p != L->pending.end(); ++p)
+            if ((*p)->ticket == ticket) {
+                L->pending.erase(p);
+                break;
+            }
+        L->live.erase(it);
+        L->cv_done.notify_all();
+    }
+    if (bytes_issued) *bytes_issued = done;
+    return DS_OK;
+}
+
+extern "C" int ds_link_wait_issued(ds_link* L, uint64_t ticket) {
+    DS_CHECK_ARG(L, "ds_link_wait_issued: NULL link");
+    std::unique_lock<std::mutex> lk(L->mu);
+    L->cv.notify_one();
+    L->cv_done.wait(lk, [&] { return L->live.find(ticket) == L->live.end(); });
+    if (L->error) return fail(L->error, "ds_link: cudaMemcpyAsync failed: %s", cudaGetErrorString((cudaError_t)L->error));
+    return DS_OK;
+}
+
+extern "C" int ds_link_idle(ds_link* L) {
+    if (!L) return 1;
+    std::lock_guard<std::mutex> g(L->mu);
+    return L->pending.empty() ? 1 : 0;
+}
+
+extern "C" int ds_link_stats(ds_link* L, uint64_t* issued, uint64_t* wasted, uint64_t* chunks) {
+    DS_CHECK_ARG(L, "ds_link_stats: NULL link");
+    std::lock_guard<std::mutex> g(L->mu);
+    if (issued) *issued = L->bytes_issued;
+    if (wasted) *wasted = L->bytes_wasted;
+    if (chunks) *chunks = L->chunks;
+    return DS_OK;
+}
+
+extern "C" int ds_link_reset_stats(ds_link* L) {
+    DS_CHECK_ARG(L, "ds_link_reset_stats: NULL link");
+    std::lock_guard<std::mutex> g(L->mu);
+    L->bytes_issued = L->bytes_wasted = L->chunks = 0;
+    return DS_OK;
+}

@@ -117,91 +117,81 @@ class ExpertCache:
 
 
 class Transfer:
-    __slots__ = ("slot", "layer", "expert", "nchunks", "next", "cancelled")
+    __slots__ = ("slot", "layer", "expert", "ticket", "cancelled")
 
-    def __init__(self, slot, layer, expert, nchunks):
-        self.slot, self.layer, self.expert, self.nchunks = slot, layer, expert, nchunks
-        self.next = 0
+    def __init__(self, slot, layer, expert, ticket):
+        self.slot, self.layer, self.expert, self.ticket = slot, layer, expert, ticket
         self.cancelled = False
-
-    @property
-    def issued(self) -> bool:
-        return self.next >= self.nchunks
 
 
 class LinkQueue:
-    """Host-side scheduler of the H2D link for decode: expert transfers are
-    split into chunks and issued just in time (at most `depth` chunks queued
-    on the copy engine), so a prefetch proven wrong by the gate (sync point 1)
-    stops after its in-flight chunks instead of occupying the link for the
-    whole expert.  With cancel=False and one chunk per expert this is exactly
-    the paper's schedule (whole-expert prefetch, then blocking re-fetch)."""
+    """Decode-side view of the native expert link (csrc/link.cu, K6).
+
+    Expert transfers are split into chunks and issued just in time by a C++
+    scheduler thread (at most `depth` chunks queued on the copy engine), so a
+    prefetch the gate proves wrong (sync point 1) is cancelled after its
+    in-flight chunks instead of holding the link for the whole expert, and
+    the link keeps streaming while the Python thread launches attention.
+    With cancel=False and one chunk per expert it is exactly the paper's
+    schedule (whole-expert prefetch, then blocking re-fetch)."""
 
     def __init__(self, cache: "ExpertCache", chunk_bytes: int, depth: int, cancel: bool):
+        import ctypes as C
+        from . import _lib
+        self.C, self.lib = C, _lib
         self.cache = cache
         blob = cache.store.blob_bytes
         self.chunk = blob if chunk_bytes <= 0 else min(chunk_bytes, blob)
-        self.nchunks = (blob + self.chunk - 1) // self.chunk
         self.depth = depth
         self.cancel_enabled = cancel
-        self.pending: list = []
-        self.inflight: list = []
-        self.wasted_bytes = 0
+        h = C.c_void_p()
+        _lib.call("ds_link_create", C.c_void_p(cache.copy_stream.cuda_stream), self.chunk, depth, C.byref(h))
+        self.handle = h
+        # materialise the slot events so their raw handles can cross the ABI
+        s = torch.cuda.current_stream(cache.device)
+        for ev in cache.ready + cache.free:
+            ev.record(s)
+        s.synchronize()
+
+    def __del__(self):
+        try:
+            self.lib.call("ds_link_destroy", self.handle)
+        except Exception:
+            pass
 
     def submit(self, slot: int, layer: int, expert: int) -> Transfer:
-        tr = Transfer(slot, layer, expert, self.nchunks)
-        self.pending.append(tr)
-        self.cache.content[slot] = (layer, expert)
-        self.pump()
-        return tr
+        c = self.cache
+        C = self.C
+        t = C.c_uint64()
+        wait = C.c_void_p(c.free[slot].cuda_event) if c.used[slot] else None
+        self.lib.call("ds_link_submit", self.handle, C.c_void_p(c.slots[slot].data_ptr()),
+                      C.c_void_p(c.store.host[layer, expert].data_ptr()), c.store.blob_bytes, wait,
+                      C.c_void_p(c.ready[slot].cuda_event), C.byref(t))
+        c.content[slot] = (layer, expert)
+        c.n_copies += 1
+        return Transfer(slot, layer, expert, t.value)
 
     def cancel(self, tr: Transfer) -> None:
-        if not self.cancel_enabled or tr.issued:
+        if not self.cancel_enabled:
             return
         tr.cancelled = True
-        self.wasted_bytes += tr.next * self.chunk
-        if tr in self.pending:
-            self.pending.remove(tr)
-
-    def _issue(self, tr: Transfer) -> None:
-        c = self.cache
-        i = tr.next
-        a = i * self.chunk
-        b = min(a + self.chunk, c.store.blob_bytes)
-        cs = c.copy_stream
-        with torch.cuda.stream(cs):
-            if i == 0 and c.used[tr.slot]:
-                cs.wait_event(c.free[tr.slot])
-            c.slots[tr.slot, a:b].copy_(c.store.host[tr.layer, tr.expert, a:b], non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(cs)
-            if i == tr.nchunks - 1:
-                c.ready[tr.slot].record(cs)
-        c.bytes_copied += b - a
-        tr.next += 1
-        self.inflight.append(ev)
-        if tr.issued:
-            c.n_copies += 1
-
-    def pump(self) -> None:
-        while self.inflight and self.inflight[0].query():
-            self.inflight.pop(0)
-        while self.pending and len(self.inflight) < self.depth:
-            tr = self.pending[0]
-            self._issue(tr)
-            if tr.issued:
-                self.pending.pop(0)
+        self.lib.call("ds_link_cancel", self.handle, tr.ticket, None)
 
     def flush(self, tr: Transfer) -> None:
-        """Block (pumping) until every chunk of tr has been issued."""
-        while not tr.issued:
-            self.pump()
-            if not tr.issued and len(self.inflight) >= self.depth:
-                self.inflight[0].synchronize()
+        """Block until every chunk of tr has been issued (its ready event recorded)."""
+        self.lib.call("ds_link_wait_issued", self.handle, tr.ticket)
 
     def wait_event(self, ev) -> None:
-        while not ev.query():
-            self.pump()
+        ev.synchronize()
+
+    def stats(self) -> dict:
+        C = self.C
+        a, b, n = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        self.lib.call("ds_link_stats", self.handle, C.byref(a), C.byref(b), C.byref(n))
+        return {"bytes_issued": a.value, "wasted_prefetch_bytes": b.value, "chunks": n.value}
+
+    def reset_stats(self) -> None:
+        self.lib.call("ds_link_reset_stats", self.handle)
 
 
 class MLPDriver:
@@ -347,9 +337,6 @@ class Engine:
         self.d2h_bytes = 0
         if hasattr(self, "link"):
             self.cache.copy_stream.synchronize()
-            self.link.pending.clear()
-            self.link.inflight.clear()
-            self.link.wasted_bytes = 0
 
     def enable_profile(self) -> "KernelProfiler":
         self.prof = KernelProfiler()
@@ -561,6 +548,10 @@ class Engine:
             self.cache.used[0] = False
         return self._link_peak
 
+    def h2d_bytes(self) -> int:
+        """Expert bytes moved host->device so far (prefill copies + decode link chunks)."""
+        return self.cache.bytes_copied + self.link.stats()["bytes_issued"]
+
     def prefill_bytes_floor(self) -> int:
         """sum_l |A_l| * expert bytes of the last prefill."""
         n = sum(len(r["activated"]) for r in self.log if r["phase"] == "prefill")
@@ -577,7 +568,7 @@ class Engine:
         exact = sum(r["pred"] == r["gate"] for r in dec)
         n = len(dec)
         return {"policy": self.policy.value, "cancel_mispredicted": self.cancel_mispredicted,
-                "chunk_bytes": self.link.chunk, "wasted_prefetch_bytes": self.link.wasted_bytes,
+                "chunk_bytes": self.link.chunk, **self.link.stats(),
                 "prefetch_hits": hits, "prefetch_misses": miss,
                 "topk_hit_rate": round(exact / n, 4) if n else None,
                 "at_least_one_rate": round(sum(bool(set(r["pred"]) & set(r["gate"])) for r in dec) / n, 4)
