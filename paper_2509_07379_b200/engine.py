@@ -193,6 +193,17 @@ class LinkQueue:
     def reset_stats(self) -> None:
         self.lib.call("ds_link_reset_stats", self.handle)
 
+    def set_chunk(self, chunk_bytes: int) -> None:
+        """Recreate the native link with a new chunk size (idle link only)."""
+        C = self.C
+        self.cache.copy_stream.synchronize()
+        self.lib.call("ds_link_destroy", self.handle)
+        self.chunk = min(chunk_bytes, self.cache.store.blob_bytes)
+        h = C.c_void_p()
+        self.lib.call("ds_link_create", C.c_void_p(self.cache.copy_stream.cuda_stream), self.chunk, self.depth,
+                      C.byref(h))
+        self.handle = h
+
 
 class MLPDriver:
     """K5 on the predict stream: P_{l+1} from the device history buffer."""
@@ -322,6 +333,8 @@ class Engine:
 
     # ------------------------------------------------------------------ API
     def reset(self) -> None:
+        if hasattr(self, "link"):
+            self.link.reset_stats()
         self.kv.len = 0
         self.log: list = []
         self.paths_decode: list = []          # recorded routing per decode token
