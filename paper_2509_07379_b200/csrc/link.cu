@@ -113,9 +113,12 @@ void worker_loop(ds_link* L) {
         if (L->pending.empty()) {
             L->cv.wait_for(lk, std::chrono::microseconds(200));
         } else {
-            // queue full: poll the oldest chunk without holding the lock
+            // queue full: spin (yielding) on the oldest chunk without holding the
+            // lock — sleep_for() has ~50 us timer slack, longer than a 4 MB chunk
             lk.unlock();
-            std::this_thread::sleep_for(std::chrono::microseconds(4));
+            const auto t0 = std::chrono::steady_clock::now();
+            while (std::chrono::steady_clock::now() - t0 < std::chrono::microseconds(2))
+                std::this_thread::yield();
             lk.lock();
         }
     }

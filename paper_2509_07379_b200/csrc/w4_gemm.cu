@@ -182,48 +182,47 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
         const size_t row_words = (size_t)K / 8;
         const W4Mat* W = args.w[e];
         const int swz = nl & 7;
-        uint4 cur[NMAT];
-        uint16_t sc[NMAT];
-        uint8_t zb[NMAT];
-        auto load = [&](int kt, uint4 (&c)[NMAT], uint16_t (&s)[NMAT], uint8_t (&z)[NMAT]) {
+        // register prefetch ring: codes/scale/zero of the next PF k-tiles are in
+        // flight while the current one is dequantised (DRAM latency ~ PF stages)
+        constexpr int PF = 4;
+        uint4 rc[PF][NMAT];
+        uint16_t rs[PF][NMAT];
+        uint8_t rz[PF][NMAT];
+        auto load = [&](int kt, uint4 (&c)[NMAT], uint16_t (&sv)[NMAT], uint8_t (&zv)[NMAT]) {
             const int kb = (kt0 + kt) * BK + 32 * half;
             const size_t gi = (size_t)n * gpr + kb / G;
 #pragma unroll
             for (int j = 0; j < NMAT; ++j) {
                 c[j] = ldg_nc_v4(W[j].codes + (size_t)n * row_words + kb / 8);
-                s[j] = __ldg(W[j].scales + gi);
-                z[j] = __ldg(W[j].zeros + (gi >> 1));
+                sv[j] = __ldg(W[j].scales + gi);
+                zv[j] = __ldg(W[j].zeros + (gi >> 1));
             }
         };
-        const size_t gi0 = 0;
-        (void)gi0;
-        uint4 nxt[NMAT];
-        uint16_t nsc[NMAT];
-        uint8_t nzb[NMAT];
-        load(0, cur, sc, zb);
-        if (KT > 1) load(1, nxt, nsc, nzb);
-        for (int kt = 0; kt < KT; ++kt) {
-            const int s = kt % STAGES;
-            if (kt >= STAGES) mbar_wait(&empty[s], ((kt / STAGES) - 1) & 1);
-            const int kb = (kt0 + kt) * BK + 32 * half;
-            const size_t gi = (size_t)n * gpr + kb / G;
-            uint8_t* a_tile = smem + s * S::STAGE_BYTES;
 #pragma unroll
-            for (int j = 0; j < NMAT; ++j) {
-                const uint32_t z = (zb[j] >> ((gi & 1) * 4)) & 15;
-                const uint32_t zz = (0x4300u | z) * 0x00010001u;
-                const uint32_t ss = (uint32_t)sc[j] * 0x00010001u;
-                dequant32(cur[j], zz, ss, a_tile + j * kTileBytes + nl * 128, 4 * half, swz);
-            }
-            fence_proxy_async_smem();
-            mbar_arrive(&full_a[s]);
+        for (int p = 0; p < PF; ++p)
+            if (p < KT) load(p, rc[p], rs[p], rz[p]);
+        for (int kb0 = 0; kb0 < KT; kb0 += PF) {
 #pragma unroll
-            for (int j = 0; j < NMAT; ++j) {
-                cur[j] = nxt[j];
-                sc[j] = nsc[j];
-                zb[j] = nzb[j];
+            for (int p = 0; p < PF; ++p) {
+                const int kt = kb0 + p;
+                if (kt < KT) {
+                    const int s = kt % STAGES;
+                    if (kt >= STAGES) mbar_wait(&empty[s], ((kt / STAGES) - 1) & 1);
+                    const int kb = (kt0 + kt) * BK + 32 * half;
+                    const size_t gi = (size_t)n * gpr + kb / G;
+                    uint8_t* a_tile = smem + s * S::STAGE_BYTES;
+#pragma unroll
+                    for (int j = 0; j < NMAT; ++j) {
+                        const uint32_t z = (rz[p][j] >> ((gi & 1) * 4)) & 15;
+                        const uint32_t zz = (0x4300u | z) * 0x00010001u;
+                        const uint32_t ss = (uint32_t)rs[p][j] * 0x00010001u;
+                        dequant32(rc[p][j], zz, ss, a_tile + j * kTileBytes + nl * 128, 4 * half, swz);
+                    }
+                    fence_proxy_async_smem();
+                    mbar_arrive(&full_a[s]);
+                    if (kt + PF < KT) load(kt + PF, rc[p], rs[p], rz[p]);
+                }
             }
-            if (kt + 2 < KT) load(kt + 2, nxt, nsc, nzb);
         }
 
         // ---------------------------------------------------------- epilogue

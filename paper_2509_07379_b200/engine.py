@@ -40,7 +40,8 @@ import torch
 
 from . import ops
 from .config import ModelShape, SchedulerPolicy, model_config_for_shape, slot_count
-from .model import DenseWeights, KVCache, attention_block, init_dense_weights, logits_last, rms_norm, rope_tables
+from .model import (DenseWeights, KVCache, attention_block, attention_decode_static, init_dense_weights,
+                    logits_last, rms_norm, rope_tables)
 from .predictor import ExpertMLP, StatsOnDevice, _mode_code
 
 
@@ -271,7 +272,7 @@ class Engine:
                  dense: DenseWeights | None = None, store: HostExpertStore | None = None,
                  predictor: ExpertMLP | None = None, pop=None, aff=None, oracle_paths=None,
                  max_seq: int = 2048, max_prefill: int = 2048, cancel_mispredicted: bool = True,
-                 chunk_mb: float = 8.0, link_depth: int = 2):
+                 chunk_mb: float = 4.0, link_depth: int = 2, use_graphs: bool = True):
         self.shape = shape
         self.policy = SchedulerPolicy(policy)
         self.device = torch.device(device)
@@ -325,6 +326,8 @@ class Engine:
         self.p_ws = torch.empty(max(ws, 256), dtype=torch.uint8, device=dev)
         self.prefill_idx_host = None
         self.capture = None          # debug/parity: list of (phase, layer, gate input, idx)
+        self.use_graphs = use_graphs
+        self.g_graphs = None
         self.prof = None             # KernelProfiler when enabled (bench)
         self.d2h_bytes = 0
         self._link_peak = None
@@ -380,14 +383,26 @@ class Engine:
     def decode_step(self) -> int:
         """One greedy decode token (feeds back the previous output token)."""
         pos = self.kv.len
-        h = self.W.embed[torch.tensor([self.token], device=self.device)]
+        if self.use_graphs:
+            self._ensure_decode_graphs()
+            self.g_pos.fill_(pos)
+            self.g_mask.copy_(torch.where(self.g_ar <= pos, 0.0, float("-inf")).view_as(self.g_mask))
+            self.g_tok.fill_(self.token)
+            self.g_h.copy_(self.W.embed.index_select(0, self.g_tok))
+        else:
+            h = self.W.embed[torch.tensor([self.token], device=self.device)]
         path = []
         if isinstance(self.driver, TraceDriver):
             self.driver.t = self.t_decode
         self._pred_next = None
         for l in range(self.L):
-            h = attention_block(self.shape, self.W.layers[l], h, self.kv, l, pos, self.cos, self.sin)
-            h, E = self._moe_decode(l, h)
+            if self.use_graphs:
+                self.g_graphs[l].replay()                          # attention + norm + K1 gate
+                ops._count("ds_gate_topk")
+                h, E = self._moe_decode(l, self.g_h1, pre=self.g_a2, out=self.g_h)
+            else:
+                h = attention_block(self.shape, self.W.layers[l], h, self.kv, l, pos, self.cos, self.sin)
+                h, E = self._moe_decode(l, h)
             path.append(tuple(E))
         self.kv.len = pos + 1
         self.paths_decode.append(tuple(path))
@@ -397,6 +412,46 @@ class Engine:
         self.token = tok
         self.t_decode += 1
         return tok
+
+    def _decode_layer_front(self, l: int) -> None:
+        """attention(l) + rms_norm + K1 gate on static buffers (captured per layer)."""
+        h1 = attention_decode_static(self.shape, self.W.layers[l], self.g_h, self.kv, l, self.g_pos, self.g_mask,
+                                     self.cos, self.sin)
+        self.g_h1.copy_(h1)
+        self.g_a2.copy_(rms_norm(h1, self.W.layers[l]["ln2"], self.shape.rms_eps))
+        ops.gate_topk(self.g_a2, self.W.layers[l]["wg"], self.k, self.idx1, self.w1, hist=self.hist, layer=l)
+
+    def _ensure_decode_graphs(self) -> None:
+        if self.g_graphs is not None:
+            return
+        dev, d = self.device, self.d
+        max_seq = self.kv.k.shape[2]
+        self.g_pos = torch.zeros(1, dtype=torch.long, device=dev)
+        self.g_tok = torch.zeros(1, dtype=torch.long, device=dev)
+        self.g_ar = torch.arange(max_seq, device=dev)
+        self.g_mask = torch.zeros((1, 1, 1, max_seq), dtype=torch.bfloat16, device=dev)
+        self.g_h = torch.zeros((1, d), dtype=torch.bfloat16, device=dev)
+        self.g_h1 = torch.zeros((1, d), dtype=torch.bfloat16, device=dev)
+        self.g_a2 = torch.zeros((1, d), dtype=torch.bfloat16, device=dev)
+        kv_k, kv_v = self.kv.k.clone(), self.kv.v.clone()
+        hist = self.hist.clone()
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            for l in range(self.L):                                 # warm-up outside capture
+                self._decode_layer_front(l)
+        torch.cuda.current_stream(dev).wait_stream(side)
+        self.g_graphs = []
+        for l in range(self.L):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                self._decode_layer_front(l)
+            self.g_graphs.append(g)
+        torch.cuda.synchronize(dev)
+        self.kv.k.copy_(kv_k)                                       # undo the warm-up writes
+        self.kv.v.copy_(kv_v)
+        self.hist.copy_(hist)
+        del kv_k, kv_v
 
     def generate(self, ids, n_new: int) -> list:
         out = [self.prefill(ids)]
@@ -475,11 +530,14 @@ class Engine:
         return out, idx_host.numpy()
 
     # --------------------------------------------------------------- decode
-    def _moe_decode(self, l: int, h: torch.Tensor):
+    def _moe_decode(self, l: int, h: torch.Tensor, pre: torch.Tensor | None = None, out: torch.Tensor | None = None):
         sh = self.shape
         link = self.link
-        a = rms_norm(h, self.W.layers[l]["ln2"], sh.rms_eps)
-        ops.gate_topk(a, self.W.layers[l]["wg"], self.k, self.idx1, self.w1, hist=self.hist, layer=l)
+        if pre is None:
+            a = rms_norm(h, self.W.layers[l]["ln2"], sh.rms_eps)
+            ops.gate_topk(a, self.W.layers[l]["wg"], self.k, self.idx1, self.w1, hist=self.hist, layer=l)
+        else:
+            a = pre                                                # gate already ran inside the layer graph
         self.ev_gate.record()
         self.idx_host.copy_(self.idx1, non_blocking=True)
         ev_idx = torch.cuda.Event()
@@ -528,7 +586,8 @@ class Engine:
             if self.prof:
                 self.prof.stop("K4 w4_swiglu_gemv+down_gemv", ev, self.store.blob_bytes)
             self.cache.release(slot_of[e])
-        out = torch.empty_like(h)
+        if out is None:
+            out = torch.empty_like(h)
         ops.combine_finalize(self.acc, h, out)
         # sync point 2: prediction for l+1 ready -> prefetch into the slots layer l-1 used
         if use_pred and l + 1 < self.L:

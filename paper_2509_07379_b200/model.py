@@ -124,5 +124,24 @@ def attention_block(shape: ModelShape, L: dict, h: torch.Tensor, kv: KVCache, la
     return (h.float() + (o @ L["wo"]).float()).to(torch.bfloat16)
 
 
+def attention_decode_static(shape: ModelShape, L: dict, h: torch.Tensor, kv: KVCache, layer: int,
+                            pos: torch.Tensor, mask: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor) -> torch.Tensor:
+    """One decode token with the position on the device (CUDA-graph capturable):
+    h [1, d]; pos int64 [1]; mask [1, 1, 1, max_seq] additive (0 for <= pos, -inf after)."""
+    nh, nkv, hd = shape.n_heads, shape.n_kv_heads, shape.head_dim
+    a = rms_norm(h, L["ln1"], shape.rms_eps)
+    q = (a @ L["wq"]).view(1, nh, hd)
+    k = (a @ L["wk"]).view(1, nkv, hd)
+    v = (a @ L["wv"]).view(1, nkv, hd)
+    c, s = cos.index_select(0, pos), sin.index_select(0, pos)
+    q, k = apply_rope(q, c, s), apply_rope(k, c, s)
+    kv.k[layer].index_copy_(1, pos, k.transpose(0, 1))
+    kv.v[layer].index_copy_(1, pos, v.transpose(0, 1))
+    o = F.scaled_dot_product_attention(q.transpose(0, 1).unsqueeze(0), kv.k[layer].unsqueeze(0),
+                                       kv.v[layer].unsqueeze(0), attn_mask=mask, enable_gqa=True)
+    o = o.squeeze(0).transpose(0, 1).reshape(1, nh * hd)
+    return (h.float() + (o @ L["wo"]).float()).to(torch.bfloat16)
+
+
 def logits_last(shape: ModelShape, W: DenseWeights, h_last: torch.Tensor) -> torch.Tensor:
     return (rms_norm(h_last, W.norm, shape.rms_eps) @ W.lm_head).float()
