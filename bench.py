@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--no-cancel", action="store_true",
                     help="paper-faithful decode: whole-expert prefetch, no cancellation of wrong prefetches")
     ap.add_argument("--chunk-mb", type=float, default=8.0)
+    ap.add_argument("--link-depth", type=int, default=2)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--out", default=None, help="also write the JSON line to this file")
     return ap.parse_args()
@@ -251,7 +252,8 @@ def run_ours(args):
     net, pop, aff = predictor_inputs(shape) if args.policy == "duoserve" else (None, None, None)
     eng = Engine(shape, args.policy if args.policy != "oracle" else "duoserve", seed=args.seed, device=dev,
                  predictor=net, pop=pop, aff=aff, max_seq=args.prefill + args.decode + 8,
-                 max_prefill=args.prefill, cancel_mispredicted=not args.no_cancel, chunk_mb=args.chunk_mb)
+                 max_prefill=args.prefill, cancel_mispredicted=not args.no_cancel, chunk_mb=args.chunk_mb,
+                 link_depth=args.link_depth)
     gen = torch.Generator().manual_seed(args.seed + 1000 * rank)
     ids_host = torch.randint(0, shape.vocab, (args.prefill,), generator=gen).pin_memory()
     if args.policy == "oracle":
@@ -261,7 +263,7 @@ def run_ours(args):
         paths = eng.paths_decode
         eng = Engine(shape, "oracle", seed=args.seed, device=dev, dense=eng.W, store=eng.store,
                      oracle_paths=paths, max_seq=args.prefill + args.decode + 8, max_prefill=args.prefill,
-                     cancel_mispredicted=not args.no_cancel, chunk_mb=args.chunk_mb)
+                     cancel_mispredicted=not args.no_cancel, chunk_mb=args.chunk_mb, link_depth=args.link_depth)
     setup_s = time.time() - t_setup
     prof = eng.enable_profile()
     eng.link_peak_gbs()
