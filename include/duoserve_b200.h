@@ -119,6 +119,11 @@ int ds_permute(const int32_t *idx, const void *x, int T, int d, int M, int k, in
  * order ("unpacks the results").  y is f32 [T*k, d].        */
 int ds_unpermute_combine(const float *y, const int32_t *pos, const float *w, const void *resid,
                          int T, int d, int k, void *out, void *stream);
+/* Expert-parallel combine term: out[t] (f32) = sum_j [owned_mask bit idx[t,j]]
+ * w[t,j] * y[pos[t*k+j]]; all-reduced across ranks then finalised with
+ * ds_combine_finalize (bit-identical to ds_unpermute_combine for k = 2).     */
+int ds_unpermute_partial(const float *y, const int32_t *pos, const float *w, const int32_t *idx,
+                         uint64_t owned_mask, int T, int d, int k, float *out, void *stream);
 /* K7: per token, hits/misses of gate set vs the resident prediction
  * (SPEC.md:386 sync point 1).  pred, idx [T,k]; miss_mask [T] bit j set
  * when idx[t,j] not in pred[t,:].                                          */

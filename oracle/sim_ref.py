@@ -33,17 +33,21 @@ def _sorted(x):
     return [int(e) for e in sorted(x)]
 
 
-def cache_log_prefill(E_by_token, L: int, policy: str = "duoserve"):
-    """E_by_token: list over prefill tokens of L-tuples of selections."""
+def cache_log_prefill(E_by_token, L: int, policy: str = "duoserve", owned=None):
+    """E_by_token: list over prefill tokens of L-tuples of selections.
+    owned: expert ids of this rank under expert parallelism (None = all);
+    the speculative first transfer is then the rank's lowest owned expert."""
     log = []
     for l in range(L):
         A = set()
         for path in E_by_token:
             A.update(path[l])
+        mine = A if owned is None else A & set(owned)
+        first = 0 if owned is None else min(owned)
         if policy in ("duoserve", "oracle"):
-            fetch = [0] + _sorted(A - {0})
+            fetch = [first] + _sorted(mine - {first})
         elif policy == "ondemand":
-            fetch = _sorted(A)
+            fetch = _sorted(mine)
         elif policy == "prefetchall":
             fetch = list(range(max(max(A) + 1, 0)))  # caller passes M via prefetchall_M
         else:
@@ -52,20 +56,23 @@ def cache_log_prefill(E_by_token, L: int, policy: str = "duoserve"):
     return log
 
 
-def cache_log_decode(paths, preds, L: int, policy: str = "duoserve"):
+def cache_log_decode(paths, preds, L: int, policy: str = "duoserve", owned=None):
     """paths[t][l] = gate selection of decode token t at layer l;
-    preds[t][l] = predicted set for l >= 1 (ignored for ondemand)."""
+    preds[t][l] = predicted set for l >= 1 (ignored for ondemand).
+    owned: expert ids of this rank under expert parallelism (None = all)."""
+    own = None if owned is None else set(owned)
+    keep = (lambda xs: _sorted(xs)) if own is None else (lambda xs: _sorted(set(xs) & own))
     log = []
     hits = misses = refetches = 0
     for t, path in enumerate(paths):
         for l in range(L):
             E = _sorted(path[l])
             if l == 0 or policy == "ondemand":
-                log.append({"phase": "decode", "token": t, "layer": l, "fetch": E, "kind": "ondemand"})
+                log.append({"phase": "decode", "token": t, "layer": l, "fetch": keep(E), "kind": "ondemand"})
                 continue
-            P = _sorted(preds[t][l])
-            miss = _sorted(set(E) - set(P))
-            hits += len(set(E) & set(P))
+            P = keep(preds[t][l])
+            miss = _sorted(set(keep(E)) - set(P))
+            hits += len(set(keep(E)) & set(P))
             misses += len(miss)
             refetches += len(miss)
             log.append({"phase": "decode", "token": t, "layer": l, "pred": P, "gate": E, "refetch": miss})

@@ -72,6 +72,7 @@ _SIGS = {
     "ds_permute": (_I, [_P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P]),
     "ds_unpermute_combine": (_I, [_P, _P, _P, _P, _I, _I, _I, _P, _P]),
     "ds_cache_check": (_I, [_P, _P, _I, _I, _P, _P]),
+    "ds_unpermute_partial": (_I, [_P, _P, _P, _P, C.c_uint64, _I, _I, _I, _P, _P]),
     "ds_route_histogram": (_I, [_P, _I, _I, _I, _I, _P, _P, _P]),
     "ds_w4_expert_layout": (_SZ, [_I, _I, _I, C.POINTER(_SZ * 9)]),
     "ds_w4_generate": (_I, [C.c_uint64, _I, _I, _I, _I, _I, _P, _P]),

@@ -175,6 +175,27 @@ __global__ void unpermute_combine_kernel(const float* __restrict__ y, const int3
     }
 }
 
+// Expert-parallel partial combine: out[t] = sum_j [expert(t,j) owned] w[t,j] y[pos[t,j]]
+// (f32, j order) — the per-rank term of the all-reduce.
+__global__ void unpermute_partial_kernel(const float* __restrict__ y, const int32_t* __restrict__ pos,
+                                         const float* __restrict__ w, const int32_t* __restrict__ idx,
+                                         unsigned long long owned, int T, int d, int k, float* __restrict__ out) {
+    const int t = blockIdx.x;
+    for (int c = threadIdx.x * 4; c < d; c += blockDim.x * 4) {
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int j = 0; j < k; ++j) {
+            if (!((owned >> idx[(size_t)t * k + j]) & 1ull)) continue;
+            const float wj = w[(size_t)t * k + j];
+            const float4 v = *reinterpret_cast<const float4*>(y + (size_t)pos[(size_t)t * k + j] * d + c);
+            acc[0] = __fadd_rn(acc[0], __fmul_rn(wj, v.x));
+            acc[1] = __fadd_rn(acc[1], __fmul_rn(wj, v.y));
+            acc[2] = __fadd_rn(acc[2], __fmul_rn(wj, v.z));
+            acc[3] = __fadd_rn(acc[3], __fmul_rn(wj, v.w));
+        }
+        *reinterpret_cast<float4*>(out + (size_t)t * d + c) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    }
+}
+
 __global__ void cache_check_kernel(const int32_t* __restrict__ idx, const int32_t* __restrict__ pred,
                                    int T, int k, int32_t* __restrict__ miss) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -253,6 +274,16 @@ extern "C" int ds_unpermute_combine(const float* y, const int32_t* pos, const fl
     unpermute_combine_kernel<<<T, 256, 0, as_stream(stream)>>>(
         y, pos, w, (const __nv_bfloat16*)resid, T, d, k, (__nv_bfloat16*)out);
     DS_LAUNCH_CHECK("ds_unpermute_combine");
+    return DS_OK;
+}
+
+extern "C" int ds_unpermute_partial(const float* y, const int32_t* pos, const float* w, const int32_t* idx,
+                                    uint64_t owned_mask, int T, int d, int k, float* out, void* stream) {
+    DS_CHECK_ARG(T >= 0 && d % 4 == 0 && k >= 1, "ds_unpermute_partial: bad shape");
+    if (T == 0) return DS_OK;
+    DS_CHECK_ARG(y && pos && w && idx && out, "ds_unpermute_partial: NULL pointer");
+    unpermute_partial_kernel<<<T, 256, 0, as_stream(stream)>>>(y, pos, w, idx, owned_mask, T, d, k, out);
+    DS_LAUNCH_CHECK("ds_unpermute_partial");
     return DS_OK;
 }
 

@@ -42,35 +42,43 @@ from . import ops
 from .config import ModelShape, SchedulerPolicy, model_config_for_shape, slot_count
 from .model import (DenseWeights, KVCache, attention_block, attention_decode_static, init_dense_weights,
                     logits_last, rms_norm, rope_tables)
+from .ep import EPConfig, owned_experts, owner_mask
 from .predictor import ExpertMLP, StatsOnDevice, _mode_code
 
 
 class HostExpertStore:
     """Pinned host memory holding every expert blob: [L, M, blob_bytes] u8."""
 
-    def __init__(self, shape: ModelShape, seed: int, device, layers: int | None = None):
+    def __init__(self, shape: ModelShape, seed: int, device, layers: int | None = None, experts=None):
+        """experts: the expert ids this process stores (expert parallelism);
+        default all M.  Non-owned experts are never allocated."""
         self.shape = shape
         self.seed = seed
         L = layers if layers is not None else shape.num_layers
         self.offsets, self.blob_bytes = ops.expert_layout(shape.hidden, shape.ffn, shape.group_size)
+        self.experts = list(range(shape.num_experts)) if experts is None else sorted(experts)
+        self.local = {e: i for i, e in enumerate(self.experts)}
         t0 = time.time()
-        self.host = torch.empty((L, shape.num_experts, self.blob_bytes), dtype=torch.uint8, pin_memory=True)
+        self.data = torch.empty((L, len(self.experts), self.blob_bytes), dtype=torch.uint8, pin_memory=True)
         self.alloc_s = time.time() - t0
         # generate on the device (counter-based, bit-identical to oracle/w4_ref.py) then D2H
         t0 = time.time()
         stage = [torch.empty(self.blob_bytes, dtype=torch.uint8, device=device) for _ in range(2)]
         s = torch.cuda.current_stream(device)
         for l in range(L):
-            for e in range(shape.num_experts):
-                buf = stage[(l * shape.num_experts + e) % 2]
+            for i, e in enumerate(self.experts):
+                buf = stage[(l * len(self.experts) + i) % 2]
                 ops.w4_generate(seed, l, e, shape.hidden, shape.ffn, shape.group_size, buf)
-                self.host[l, e].copy_(buf, non_blocking=True)
+                self.data[l, i].copy_(buf, non_blocking=True)
         s.synchronize()
         self.fill_s = time.time() - t0
 
+    def blob(self, layer: int, expert: int) -> torch.Tensor:
+        return self.data[layer, self.local[expert]]
+
     @property
     def nbytes(self) -> int:
-        return self.host.numel()
+        return self.data.numel()
 
 
 class ExpertCache:
@@ -101,7 +109,7 @@ class ExpertCache:
         with torch.cuda.stream(self.copy_stream):
             if self.used[slot]:
                 self.copy_stream.wait_event(self.free[slot])
-            self.slots[slot].copy_(self.store.host[layer, expert], non_blocking=True)
+            self.slots[slot].copy_(self.store.blob(layer, expert), non_blocking=True)
             self.ready[slot].record(self.copy_stream)
         self.content[slot] = (layer, expert)
         self.bytes_copied += self.store.blob_bytes
@@ -166,7 +174,7 @@ class LinkQueue:
         t = C.c_uint64()
         wait = C.c_void_p(c.free[slot].cuda_event) if c.used[slot] else None
         self.lib.call("ds_link_submit", self.handle, C.c_void_p(c.slots[slot].data_ptr()),
-                      C.c_void_p(c.store.host[layer, expert].data_ptr()), c.store.blob_bytes, wait,
+                      C.c_void_p(c.store.blob(layer, expert).data_ptr()), c.store.blob_bytes, wait,
                       C.c_void_p(c.ready[slot].cuda_event), C.byref(t))
         c.content[slot] = (layer, expert)
         c.n_copies += 1
@@ -272,7 +280,8 @@ class Engine:
                  dense: DenseWeights | None = None, store: HostExpertStore | None = None,
                  predictor: ExpertMLP | None = None, pop=None, aff=None, oracle_paths=None,
                  max_seq: int = 2048, max_prefill: int = 2048, cancel_mispredicted: bool = True,
-                 chunk_mb: float = 4.0, link_depth: int = 2, use_graphs: bool = True):
+                 chunk_mb: float = 4.0, link_depth: int = 2, use_graphs: bool = True,
+                 ep: EPConfig | None = None):
         self.shape = shape
         self.policy = SchedulerPolicy(policy)
         self.device = torch.device(device)
@@ -282,7 +291,10 @@ class Engine:
         self.W = dense if dense is not None else init_dense_weights(sh, seed, device=self.device)
         if self.W.embed.device != self.device:
             self.W = self.W.to(self.device)
-        self.store = store if store is not None else HostExpertStore(sh, seed, self.device)
+        self.ep = ep
+        self.owned = owned_experts(sh.num_experts, ep.rank, ep.world) if ep else list(range(sh.num_experts))
+        self.owned_set = set(self.owned)
+        self.store = store if store is not None else HostExpertStore(sh, seed, self.device, experts=self.owned)
         cfg = model_config_for_shape(sh)
         self.n_slots = slot_count(self.policy, cfg)
         self.cache = ExpertCache(self.store, self.n_slots, self.device)
@@ -322,6 +334,8 @@ class Engine:
         self.p_xperm = torch.empty((P * self.k, self.d), dtype=torch.bfloat16, device=dev)
         self.p_h = torch.empty((P * self.k, self.ff), dtype=torch.bfloat16, device=dev)
         self.p_y = torch.empty((P * self.k, self.d), dtype=torch.float32, device=dev)
+        self.owner_bits = owner_mask(self.M, ep.rank, ep.world) if ep else (1 << self.M) - 1
+        self.p_part = torch.zeros((P, self.d), dtype=torch.float32, device=dev) if ep else None
         ws = max(ops.grouped_ffn_workspace(r, self.d, self.ff) for r in (P * self.k // 4, P * self.k))
         self.p_ws = torch.empty(max(ws, 256), dtype=torch.uint8, device=dev)
         self.prefill_idx_host = None
@@ -471,8 +485,9 @@ class Engine:
             self._spec = None
             return
         slot = self._next_ring_slot()
-        self.cache.load(slot, layer, 0)
-        self._spec = (slot, layer, 0)
+        first = self.owned[0]                    # lowest (owned) expert; 0 on a single GPU
+        self.cache.load(slot, layer, first)
+        self._spec = (slot, layer, first)
 
     def _moe_prefill(self, l: int, h: torch.Tensor, T: int):
         sh = self.shape
@@ -491,7 +506,8 @@ class Engine:
         done.synchronize()                                  # activated set -> host
         self.d2h_bytes += self.p_off_host.nbytes + idx_host.nbytes
         off = self.p_off_host.tolist()
-        A = [e for e in range(self.M) if off[e + 1] > off[e]]
+        A_all = [e for e in range(self.M) if off[e + 1] > off[e]]
+        A = [e for e in A_all if e in self.owned_set]       # this rank's share (all on one GPU)
         plan = []                                           # (expert, slot, already_queued)
         if self.policy is SchedulerPolicy.ON_DEMAND:
             plan = [(e, i % self.n_slots, False) for i, e in enumerate(A)]
@@ -500,7 +516,7 @@ class Engine:
             if spec is not None:
                 plan.append((spec[2], spec[0], True))
             plan += [(e, self._next_ring_slot(), False) for e in A if not (spec and e == spec[2])]
-        self.log.append({"phase": "prefill", "layer": l, "fetch": [e for e, _, _ in plan], "activated": A})
+        self.log.append({"phase": "prefill", "layer": l, "fetch": [e for e, _, _ in plan], "activated": A_all})
         # sliding window over the slot ring: the copy into a slot is queued only
         # after the compute that last used it has been queued (its free event)
         window = self.n_slots if self.policy is not SchedulerPolicy.ON_DEMAND else self.n_slots
@@ -526,7 +542,13 @@ class Engine:
         # next layer's first expert streams while this layer combines + next attention runs
         self._spec_fetch(l + 1)
         out = torch.empty_like(h)
-        ops.unpermute_combine(self.p_y[:T * self.k], self.p_pos[:T * self.k], w, h, out)
+        if self.ep is None:
+            ops.unpermute_combine(self.p_y[:T * self.k], self.p_pos[:T * self.k], w, h, out)
+        else:
+            part = self.p_part[:T]
+            ops.unpermute_partial(self.p_y[:T * self.k], self.p_pos[:T * self.k], w, idx, self.owner_bits, part)
+            self.ep.all_reduce_(part)                       # sum of the ranks' expert terms
+            ops.combine_finalize(part, h, out)
         return out, idx_host.numpy()
 
     # --------------------------------------------------------------- decode
@@ -552,31 +574,36 @@ class Engine:
             self.capture.append(("decode", l, a.cpu(), self.idx_host.clone()))
         slot_of, trs = {}, {}
         miss = []
+        mine = [e for e in E if e in self.owned_set]
         if l == 0 or not use_pred:
             base = 0 if (l % 2 == 0 or self.n_slots < 2 * self.k) else self.k
-            for j, e in enumerate(E):
+            for j, e in enumerate(mine):
                 slot = (base + j) % self.n_slots
                 trs[e] = link.submit(slot, l, e)
                 slot_of[e] = slot
-            self.log.append({"phase": "decode", "token": self.t_decode, "layer": l, "fetch": E,
+            self.log.append({"phase": "decode", "token": self.t_decode, "layer": l, "fetch": mine,
                              "kind": "ondemand"})
         else:
-            P, order, pending = self._pred_next
-            miss = sorted(set(E) - set(P))
-            wrong = [p for p in order if p not in E]
+            P, order, pending = self._pred_next              # pending: this rank's predicted experts
+            miss = sorted(set(mine) - set(P))
+            spare = [pending[p][0] for p in order if p in pending and p not in E]
             for p in order:
+                if p not in pending:
+                    continue
                 if p in E:
                     slot_of[p], trs[p] = pending[p]
                 else:
-                    link.cancel(pending[p][1])                     # drop its not-yet-issued chunks
-            for e, p in zip(miss, wrong):
-                s_ = pending[p][0]
-                trs[e] = link.submit(s_, l, e)                     # re-fetch into the wrong slot
+                    link.cancel(pending[p][1])                 # drop its not-yet-issued chunks
+            used = set(slot_of.values())
+            spare += [s_ for s_ in range(self.n_slots) if s_ not in used and s_ not in spare]
+            for e, s_ in zip(miss, spare):
+                trs[e] = link.submit(s_, l, e)                 # re-fetch into a wrong (or free) slot
                 slot_of[e] = s_
-            self.log.append({"phase": "decode", "token": self.t_decode, "layer": l, "pred": sorted(P),
+            self.log.append({"phase": "decode", "token": self.t_decode, "layer": l,
+                             "pred": sorted(p for p in P if p in self.owned_set),
                              "gate": sorted(E), "refetch": miss})
         # expert compute: hits first (already resident or in flight), then re-fetched ones
-        for e in [x for x in E if x not in miss] + miss:
+        for e in [x for x in mine if x not in miss] + miss:
             j = E.index(e)
             link.flush(trs[e])
             st = self.cache.acquire(slot_of[e])
@@ -588,6 +615,8 @@ class Engine:
             self.cache.release(slot_of[e])
         if out is None:
             out = torch.empty_like(h)
+        if self.ep is not None:
+            self.ep.all_reduce_(self.acc)                      # sum of the ranks' expert terms
         ops.combine_finalize(self.acc, h, out)
         # sync point 2: prediction for l+1 ready -> prefetch into the slots layer l-1 used
         if use_pred and l + 1 < self.L:
@@ -595,7 +624,7 @@ class Engine:
             cur = set(slot_of.values())
             free = [s_ for s_ in range(self.n_slots) if s_ not in cur][: self.k]
             pending = {}
-            for e, s_ in zip(order, free):
+            for e, s_ in zip([e for e in order if e in self.owned_set], free):
                 pending[e] = (s_, link.submit(s_, l + 1, e))
             self._pred_next = (Pn, order, pending)
         return out, E
@@ -604,7 +633,7 @@ class Engine:
     def link_peak_gbs(self) -> float:
         """Measured pinned H2D bandwidth (copy engine), 1 expert blob x 16."""
         if self._link_peak is None:
-            src = self.store.host[0, 0]
+            src = self.store.data[0, 0]
             dst = self.cache.slots[0]
             s = self.cache.copy_stream
             with torch.cuda.stream(s):

@@ -1,0 +1,85 @@
+"""Expert parallelism: the M experts of every layer are
+sharded over G ranks (rank r owns experts e with e % G == r); each rank holds
+only its shard in pinned host memory, its own `slot_count` HBM cache and its
+own copy stream / link, so the aggregate host-link bandwidth grows with G.
+
+Attention, norms and the gate stay replicated (batch-1 serving: every rank
+sees the same tokens, and the deterministic kernels give the same routing on
+every rank).  Each rank computes the routing-weighted sum of ITS selected
+experts into an f32 partial [T, d]; one all-reduce (NCCL over NVLink on B200;
+gloo in the CPU tests) combines them.  With top-k = 2 at most two ranks hold a
+non-zero term per element and adding exact zeros is exact, so the EP result is
+bit-identical to the single-GPU result (tests/test_ep.py).
+
+The reference is single-GPU by design; this is
+the scaling extension named in BASELINE.json's north star.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+
+def owner(expert: int, world: int) -> int:
+    return expert % world
+
+
+def owned_experts(M: int, rank: int, world: int) -> list:
+    return [e for e in range(M) if owner(e, world) == rank]
+
+
+def owner_mask(M: int, rank: int, world: int) -> int:
+    m = 0
+    for e in owned_experts(M, rank, world):
+        m |= 1 << e
+    return m
+
+
+def shard_fetch(fetch: list, rank: int, world: int) -> list:
+    """The part of a (single-GPU) fetch list this rank performs."""
+    return [e for e in fetch if owner(e, world) == rank]
+
+
+def shard_log(log: list, rank: int, world: int) -> list:
+    """Restrict a single-GPU cache log to the transfers owned by `rank`:
+    prefill fetch lists, decode on-demand fetches, predictions and re-fetches
+    are filtered by ownership; the gate sets stay whole (replicated routing)."""
+    out = []
+    for r in log:
+        r = dict(r)
+        for key in ("fetch", "pred", "refetch"):
+            if key in r:
+                r[key] = shard_fetch(r[key], rank, world)
+        out.append(r)
+    return out
+
+
+@dataclass
+class EPConfig:
+    rank: int
+    world: int
+    group: object = None          # torch.distributed ProcessGroup (None = default group)
+
+    @classmethod
+    def from_env(cls) -> "EPConfig | None":
+        import torch.distributed as dist
+        if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
+            return None
+        return cls(dist.get_rank(), dist.get_world_size(), None)
+
+    def all_reduce_(self, t: torch.Tensor) -> torch.Tensor:
+        """In-place SUM all-reduce (NCCL over NVLink for CUDA tensors; a gloo
+        group stages CUDA tensors through host memory)."""
+        import torch.distributed as dist
+        if t.is_cuda and dist.get_backend(self.group) == "gloo":
+            h = t.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.SUM, group=self.group)
+            t.copy_(h)
+        else:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        return t
+
+    def owns(self, expert: int) -> bool:
+        return owner(expert, self.world) == self.rank

@@ -72,6 +72,13 @@ def unpermute_combine(y: torch.Tensor, pos, w, resid, out) -> None:
     _count("ds_unpermute_combine")
 
 
+def unpermute_partial(y: torch.Tensor, pos, w, idx, owned_mask: int, out: torch.Tensor) -> None:
+    T, k = w.shape
+    _lib.call("ds_unpermute_partial", ptr(y), ptr(pos), ptr(w), ptr(idx), owned_mask, T, out.shape[1], k, ptr(out),
+              stream_ptr())
+    _count("ds_unpermute_partial")
+
+
 def swiglu_gemv(x: torch.Tensor, e: _lib.W4Expert, d: int, ff: int, G: int, h: torch.Tensor) -> None:
     _lib.call("ds_w4_swiglu_gemv", ptr(x), x.shape[0], C.byref(e), d, ff, G, ptr(h), stream_ptr())
     _count("ds_w4_swiglu_gemv", (x.shape[0] + 3) // 4)

@@ -1,0 +1,79 @@
+"""Expert-parallel engine, world_size 2, on the one GPU of the box (gloo
+process group; on a multi-GPU box the same code runs NCCL over NVLink).
+Tokens must equal the single-GPU run (the EP combine is bit-identical) and
+each rank's cache log must equal the sharded SPEC-simulator log."""
+
+import os
+import socket
+
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+PREFILL, DECODE = 32, 6
+
+
+def _setup(dev):
+    from paper_2509_07379_b200 import config as C, predictor as P, stats as S, trace as T
+    from paper_2509_07379_b200.model import init_dense_weights
+    shape = C.load_shape("tiny-4x8")
+    cfg, _ = C.load_preset("tiny-4x8")
+    ds = T.generate_traces(T.default_generator_params(4, 8, 0.8, seed=7), cfg, 4, 8, 8)
+    pop, aff = S.build_popularity(ds), S.build_affinity(ds)
+    net = P.ExpertMLP(P.feature_length(4, 8, 2), 8, seed=0, meta={"L": 4, "M": 8, "k": 2})
+    dense = init_dense_weights(shape, seed=1, device="cpu").to(dev)
+    ids = torch.randint(0, shape.vocab, (PREFILL,), generator=torch.Generator().manual_seed(0))
+    return shape, net, pop, aff, dense, ids
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+    from paper_2509_07379_b200.engine import Engine
+    from paper_2509_07379_b200.ep import EPConfig
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dev = torch.device("cuda:0")
+    shape, net, pop, aff, dense, ids = _setup(dev)
+    eng = Engine(shape, "duoserve", seed=3, dense=dense, predictor=net, pop=pop, aff=aff, max_seq=64,
+                 max_prefill=PREFILL, ep=EPConfig(rank, world))
+    toks = eng.generate(ids, DECODE)
+    q.put((rank, toks, eng.log, [list(map(list, p)) for p in eng.paths_decode], eng.paths_prefill.tolist(),
+           eng.store.experts))
+    dist.destroy_process_group()
+
+
+def test_ep_world2_matches_single_gpu(cuda):
+    from oracle import predictor_ref, sim_ref
+    from paper_2509_07379_b200.engine import Engine
+    shape, net, pop, aff, dense, ids = _setup(cuda)
+    single = Engine(shape, "duoserve", seed=3, dense=dense, predictor=net, pop=pop, aff=aff, max_seq=64,
+                    max_prefill=PREFILL)
+    ref_toks = single.generate(ids, DECODE)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=600) for _ in procs], key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=120)
+    L = shape.num_layers
+    ref_net = predictor_ref.RefNet(net.input_dim, 8, net.hidden, 0)
+    for rank, toks, log, dpaths, ppaths, experts in res:
+        assert toks == ref_toks
+        assert experts == [e for e in range(8) if e % 2 == rank]
+        pre = [tuple(tuple(x) for x in ppaths[t]) for t in range(PREFILL)]
+        dec = [tuple(tuple(x) for x in p) for p in dpaths]
+        preds = []
+        for path in dec:
+            sets, _ = predictor_ref.predict_sets(ref_net, [path] * (L - 1), list(range(1, L)), pop.values,
+                                                 aff.values, 2)
+            preds.append([None] + [tuple(x) for x in sets])
+        exp = sim_ref.cache_log_prefill(pre, L, owned=experts) + \
+            sim_ref.cache_log_decode(dec, preds, L, owned=experts)[0]
+        assert log == exp, rank
