@@ -78,7 +78,7 @@ __global__ void dequant_kernel(const uint32_t* __restrict__ codes, const uint16_
 }
 
 // -------------------------------------------------------------- GEMV (K4)
-constexpr int kGemvThreads = 256;
+constexpr int kGemvThreads = 512;
 constexpr int kRMax = 4;  // activation rows per pass (decode batch chunk)
 
 struct W4Ptr {
@@ -96,10 +96,11 @@ __device__ __forceinline__ int swz_unit(int u) { return u ^ ((u >> 3) & 3); }
 __device__ __forceinline__ void stage_x(const __nv_bfloat16* __restrict__ x, int R, int K,
                                         uint32_t* xs, float* xsum) {
     const int words = K / 2;
-    const uint32_t* xw = reinterpret_cast<const uint32_t*>(x);
-    for (int i = threadIdx.x; i < R * words; i += blockDim.x) {
-        const int r = i / words, w = i - r * words;
-        xs[r * words + swz_unit(w >> 2) * 4 + (w & 3)] = __ldg(xw + i);
+    const int units = words / 4;                        // 16-byte units per row
+    const uint4* xu = reinterpret_cast<const uint4*>(x);
+    for (int i = threadIdx.x; i < R * units; i += blockDim.x) {
+        const int r = i / units, u = i - r * units;
+        *reinterpret_cast<uint4*>(xs + r * words + swz_unit(u) * 4) = __ldg(xu + i);
     }
     __syncthreads();
     const int chunks = K / 32;
@@ -202,7 +203,7 @@ __global__ void __launch_bounds__(kGemvThreads) swiglu_gemv_kernel(
     const W4Ptr W[2] = {w1, w3};
     for (int n = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); n < N; n += warps) {
         float acc[2][R];
-        gemv_row<R, 2, 2>(W, n, K, G, xs, xsum, acc);
+        gemv_row<R, 2, (R == 1 ? 4 : 2)>(W, n, K, G, xs, xsum, acc);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             if (lane == r) {
@@ -227,7 +228,7 @@ __global__ void __launch_bounds__(kGemvThreads) down_gemv_kernel(
     const W4Ptr W[1] = {w2};
     for (int n = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); n < N; n += warps) {
         float acc[1][R];
-        gemv_row<R, 1, 4>(W, n, K, G, xs, xsum, acc);
+        gemv_row<R, 1, (R == 1 ? 8 : 4)>(W, n, K, G, xs, xsum, acc);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             if (lane == r) {

@@ -10,13 +10,16 @@
 // small per-expert row counts still fill M=128 tiles.
 //
 // Per CTA (one 128 x BN output tile, one expert):
-//   warp 0      TMA producer: activation tile [BN x 64] bf16, SWIZZLE_128B
+//   warp 0      TMA producer: activation tile [BN x 64] bf16 (SWIZZLE_128B)
+//               and the packed int4 code tiles [128 rows x 32 B] of W1/W3
+//               (or W2) for the same k-range, all on one mbarrier
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
 //               (kind::f16, f32 accumulators in TMEM: NMAT x BN columns)
-//   warps 2-9   W4 dequant producers: 16-byte streaming loads of packed int4
-//               codes, w = bf16((q - z) * s) via the bf16 exponent trick +
-//               HSUB2/HMUL2 (bit-identical to ds_w4_dequant), written into
-//               the UMMA K-major SWIZZLE_128B layout, fence.proxy.async, arrive
+//   warps 2-9   W4 dequant: codes from shared memory, group scales/zeros
+//               staged once per CTA in shared memory, w = bf16((q - z) * s)
+//               via the bf16 exponent trick + HSUB2/HMUL2 (bit-identical to
+//               ds_w4_dequant), written into the UMMA K-major SWIZZLE_128B
+//               layout, fence.proxy.async, arrive
 //   warps 2-5   epilogue: tcgen05.ld TMEM -> registers -> SwiGLU -> global
 // Stages are tied by mbarriers: full_b (TMA tx bytes), full_a (256 dequant
 // arrivals), empty (tcgen05.commit), tmem_full (final commit).
@@ -46,6 +49,7 @@ struct W4Mat {
 };
 
 struct GemmArgs {
+    CUtensorMap codes_map[kMaxExperts][2];   // [N, K/2] u8 tiles {32 B, 128 rows}
     int K, N, G;
     int kt_per_split;   // k-tiles (of BK) per split
     int splits;
@@ -56,13 +60,21 @@ struct GemmArgs {
     void* out;          // NMAT=2: bf16 H [total_rows, N]; NMAT=1: f32 [splits][total_rows][N]
 };
 
+constexpr int kCodeTile = BM * (BK / 2);   // 128 rows x 32 B of packed codes
+constexpr int kMaxGroupsPerCta = 64;       // staged scales/zeros per row (K-range / G)
+
 template <int NMAT>
 struct Smem {
     static constexpr int STAGES = NMAT == 2 ? 3 : 4;
     static constexpr int A_BYTES = NMAT * kTileBytes;
     static constexpr int B_BYTES = BN * 128;
-    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+    static constexpr int C_BYTES = NMAT * kCodeTile;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES + C_BYTES;
+    static constexpr int SC_OFF = STAGES * STAGE_BYTES;                    // bf16 scales [NMAT][128][groups]
+    static constexpr int SC_BYTES = NMAT * BM * kMaxGroupsPerCta * 2;
+    static constexpr int Z_OFF = SC_OFF + SC_BYTES;                        // u8 zeros [NMAT][128][groups]
+    static constexpr int Z_BYTES = NMAT * BM * kMaxGroupsPerCta;
+    static constexpr int BAR_OFF = Z_OFF + Z_BYTES;
     static constexpr int TOTAL = BAR_OFF + 256 + 1024;  // + barriers + alignment slack
 };
 
@@ -126,6 +138,7 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
         mbar_init(tmem_full, 1);
         fence_mbar_init();
         tma_prefetch_desc(&act_map);
+        for (int j = 0; j < NMAT; ++j) tma_prefetch_desc(&args.codes_map[e][j]);
     }
     if (warp == 1) tmem_alloc<TMEM_COLS>(tmem_slot);
     tc_fence_before();
@@ -141,8 +154,12 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
                 const int s = kt % STAGES;
                 if (kt >= STAGES) mbar_wait(&empty[s], ((kt / STAGES) - 1) & 1);
                 uint8_t* b_tile = smem + s * S::STAGE_BYTES + S::A_BYTES;
-                mbar_expect_tx(&full_b[s], S::B_BYTES);
+                uint8_t* c_tile = b_tile + S::B_BYTES;
+                mbar_expect_tx(&full_b[s], S::B_BYTES + S::C_BYTES);
                 tma_load_2d(b_tile, &act_map, &full_b[s], (kt0 + kt) * BK, row_coord);
+#pragma unroll
+                for (int j = 0; j < NMAT; ++j)
+                    tma_load_2d(c_tile + j * kCodeTile, &args.codes_map[e][j], &full_b[s], (kt0 + kt) * (BK / 2), n0);
             }
         }
     } else if (warp == 1) {
@@ -175,54 +192,39 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
     } else {
         // ------------------------------------------------ dequant producers
         const int t = threadIdx.x - 64;          // 0..255
-        const int nl = t & 127, half = t >> 7;
-        const int n = n0 + nl;
+        const int nl = t >> 1, half = t & 1;     // 2 threads per weight row (32 codes each)
         const int K = args.K, G = args.G;
         const int gpr = K / G;
-        const size_t row_words = (size_t)K / 8;
+        const int g0 = kt0 * BK / G;             // first group of this CTA's k-range
+        const int ng = KT * BK / G;              // groups in the k-range (<= kMaxGroupsPerCta)
         const W4Mat* W = args.w[e];
+        uint16_t* sc_s = reinterpret_cast<uint16_t*>(smem + S::SC_OFF);
+        uint8_t* z_s = smem + S::Z_OFF;
+        // stage the n-block's scales and zeros for the whole k-range once
+        for (int i = t; i < NMAT * BM * ng; i += kDequantThreads) {
+            const int j = i / (BM * ng), rem = i - j * BM * ng, r = rem / ng, g = rem - r * ng;
+            const size_t gi = (size_t)(n0 + r) * gpr + g0 + g;
+            sc_s[(j * BM + r) * kMaxGroupsPerCta + g] = __ldg(W[j].scales + gi);
+            z_s[(j * BM + r) * kMaxGroupsPerCta + g] = (__ldg(W[j].zeros + (gi >> 1)) >> ((gi & 1) * 4)) & 15;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kDequantThreads));
         const int swz = nl & 7;
-        // register prefetch ring: codes/scale/zero of the next PF k-tiles are in
-        // flight while the current one is dequantised (DRAM latency ~ PF stages)
-        constexpr int PF = 4;
-        uint4 rc[PF][NMAT];
-        uint16_t rs[PF][NMAT];
-        uint8_t rz[PF][NMAT];
-        auto load = [&](int kt, uint4 (&c)[NMAT], uint16_t (&sv)[NMAT], uint8_t (&zv)[NMAT]) {
-            const int kb = (kt0 + kt) * BK + 32 * half;
-            const size_t gi = (size_t)n * gpr + kb / G;
+        for (int kt = 0; kt < KT; ++kt) {
+            const int s = kt % STAGES;
+            mbar_wait(&full_b[s], (kt / STAGES) & 1);            // codes (and B) landed
+            uint8_t* stage = smem + s * S::STAGE_BYTES;
+            const uint8_t* c_tile = stage + S::A_BYTES + S::B_BYTES;
+            const int g = (kt * BK + 32 * half) / G;
 #pragma unroll
             for (int j = 0; j < NMAT; ++j) {
-                c[j] = ldg_nc_v4(W[j].codes + (size_t)n * row_words + kb / 8);
-                sv[j] = __ldg(W[j].scales + gi);
-                zv[j] = __ldg(W[j].zeros + (gi >> 1));
+                const uint4 c = *reinterpret_cast<const uint4*>(c_tile + j * kCodeTile + nl * 32 + half * 16);
+                const uint32_t z = z_s[(j * BM + nl) * kMaxGroupsPerCta + g];
+                const uint32_t zz = (0x4300u | z) * 0x00010001u;
+                const uint32_t ss = (uint32_t)sc_s[(j * BM + nl) * kMaxGroupsPerCta + g] * 0x00010001u;
+                dequant32(c, zz, ss, stage + j * kTileBytes + nl * 128, 4 * half, swz);
             }
-        };
-#pragma unroll
-        for (int p = 0; p < PF; ++p)
-            if (p < KT) load(p, rc[p], rs[p], rz[p]);
-        for (int kb0 = 0; kb0 < KT; kb0 += PF) {
-#pragma unroll
-            for (int p = 0; p < PF; ++p) {
-                const int kt = kb0 + p;
-                if (kt < KT) {
-                    const int s = kt % STAGES;
-                    if (kt >= STAGES) mbar_wait(&empty[s], ((kt / STAGES) - 1) & 1);
-                    const int kb = (kt0 + kt) * BK + 32 * half;
-                    const size_t gi = (size_t)n * gpr + kb / G;
-                    uint8_t* a_tile = smem + s * S::STAGE_BYTES;
-#pragma unroll
-                    for (int j = 0; j < NMAT; ++j) {
-                        const uint32_t z = (rz[p][j] >> ((gi & 1) * 4)) & 15;
-                        const uint32_t zz = (0x4300u | z) * 0x00010001u;
-                        const uint32_t ss = (uint32_t)rs[p][j] * 0x00010001u;
-                        dequant32(rc[p][j], zz, ss, a_tile + j * kTileBytes + nl * 128, 4 * half, swz);
-                    }
-                    fence_proxy_async_smem();
-                    mbar_arrive(&full_a[s]);
-                    if (kt + PF < KT) load(kt + PF, rc[p], rs[p], rz[p]);
-                }
-            }
+            fence_proxy_async_smem();
+            mbar_arrive(&full_a[s]);
         }
 
         // ---------------------------------------------------------- epilogue
@@ -296,6 +298,20 @@ EncodeTiledFn encode_fn() {
     return fn;
 }
 
+int make_codes_map(CUtensorMap* map, const void* codes, int N, int K) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return fail(DS_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {(cuuint64_t)K / 2, (cuuint64_t)N};
+    cuuint64_t strides[1] = {(cuuint64_t)K / 2};
+    cuuint32_t box[2] = {BK / 2, BM};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(codes), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(DS_ERR_ARG, "cuTensorMapEncodeTiled (codes) failed (%d)", (int)r);
+    return DS_OK;
+}
+
 int make_act_map(CUtensorMap* map, const void* base, int rows, int K) {
     EncodeTiledFn fn = encode_fn();
     if (!fn) return fail(DS_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
@@ -332,16 +348,26 @@ int launch_gemm(const CUtensorMap& map, const GemmArgs& a, int E, int max_mblock
     return DS_OK;
 }
 
+int splits_for(int d, int ff, int G, int mblocks) {
+    int splits = choose_splits(d, mblocks);
+    while (splits > 1 && (ff / BK) % splits) splits >>= 1;
+    while (splits < 8 && (ff / splits) / G > kMaxGroupsPerCta) splits <<= 1;   // staged-scale capacity
+    return splits;
+}
+
 }  // namespace
 }  // namespace ds
 
 using namespace ds;
 
 extern "C" size_t ds_w4_grouped_ffn_workspace(int total_rows, int d, int ff) {
-    (void)ff;
     const int mb = (total_rows + BN - 1) / BN;
-    return (size_t)choose_splits(d, mb) * total_rows * d * sizeof(float);
+    const int s = ds::splits_for(d, ff, 64, mb) > ds::splits_for(d, ff, 128, mb) ? ds::splits_for(d, ff, 64, mb)
+                                                                               : ds::splits_for(d, ff, 128, mb);
+    return (size_t)s * total_rows * d * sizeof(float);
 }
+
+
 
 extern "C" int ds_w4_grouped_ffn(const void* xperm, const int32_t* offsets, int E,
                                  const ds_w4_expert* experts, int d, int ff, int G, void* h, float* y,
@@ -350,6 +376,7 @@ extern "C" int ds_w4_grouped_ffn(const void* xperm, const int32_t* offsets, int 
     DS_CHECK_ARG(d % BM == 0 && ff % BM == 0 && d % BK == 0 && ff % BK == 0,
                  "ds_w4_grouped_ffn: d, ff must be multiples of 128");
     DS_CHECK_ARG(G == 64 || G == 128, "ds_w4_grouped_ffn: G must be 64 or 128");
+    DS_CHECK_ARG(d / G <= kMaxGroupsPerCta, "ds_w4_grouped_ffn: d / G must be <= %d", kMaxGroupsPerCta);
     DS_CHECK_ARG(xperm && offsets && experts && h && y, "ds_w4_grouped_ffn: NULL pointer");
     const int total_rows = offsets[E];
     GemmArgs a1{}, a2{};
@@ -370,6 +397,12 @@ extern "C" int ds_w4_grouped_ffn(const void* xperm, const int32_t* offsets, int 
         a2.w[i][0] = W4Mat{L[2]->codes, (const uint16_t*)L[2]->scales, L[2]->zeros};
     }
     if (total_rows == 0 || max_mb == 0) return DS_OK;
+    for (int i = 0; i < E; ++i) {
+        int rc0 = make_codes_map(&a1.codes_map[i][0], experts[i].w1.codes, ff, d);
+        if (!rc0) rc0 = make_codes_map(&a1.codes_map[i][1], experts[i].w3.codes, ff, d);
+        if (!rc0) rc0 = make_codes_map(&a2.codes_map[i][0], experts[i].w2.codes, d, ff);
+        if (rc0) return rc0;
+    }
     cudaStream_t st = as_stream(stream);
     // GEMM1: K = d, N = ff
     CUtensorMap map1, map2;
@@ -382,8 +415,7 @@ extern "C" int ds_w4_grouped_ffn(const void* xperm, const int32_t* offsets, int 
     // GEMM2: K = ff, N = d, split-K with a deterministic reduction
     rc = make_act_map(&map2, h, total_rows, ff);
     if (rc) return rc;
-    int splits = choose_splits(d, mb_total);
-    while (splits > 1 && (ff / BK) % splits) splits >>= 1;
+    const int splits = splits_for(d, ff, G, mb_total);
     const size_t need = (size_t)splits * total_rows * d * sizeof(float);
     a2.K = ff; a2.N = d; a2.G = G; a2.kt_per_split = (ff / BK) / splits; a2.splits = splits;
     a2.total_rows = total_rows;
