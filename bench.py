@@ -301,8 +301,10 @@ def run_ours(args):
     torch.cuda.synchronize()
     res = []
     with ClockSampler(lr) as clk:
+        torch.cuda.nvtx.range_push("timed")          # ncu --nvtx --nvtx-include "timed/"
         for _ in range(args.steps):
             res.append(one_step(args.decode))
+        torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()

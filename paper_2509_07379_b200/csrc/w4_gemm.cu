@@ -195,8 +195,8 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
         const int nl = t >> 1, half = t & 1;     // 2 threads per weight row (32 codes each)
         const int K = args.K, G = args.G;
         const int gpr = K / G;
-        const int g0 = kt0 * BK / G;             // first group of this CTA's k-range
-        const int ng = KT * BK / G;              // groups in the k-range (<= kMaxGroupsPerCta)
+        const int g0 = kt0 * BK / G;             // first group touching this CTA's k-range
+        const int ng = ((kt0 + KT) * BK + G - 1) / G - g0;   // groups touched (<= kMaxGroupsPerCta)
         const W4Mat* W = args.w[e];
         uint16_t* sc_s = reinterpret_cast<uint16_t*>(smem + S::SC_OFF);
         uint8_t* z_s = smem + S::Z_OFF;
@@ -214,7 +214,7 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
             mbar_wait(&full_b[s], (kt / STAGES) & 1);            // codes (and B) landed
             uint8_t* stage = smem + s * S::STAGE_BYTES;
             const uint8_t* c_tile = stage + S::A_BYTES + S::B_BYTES;
-            const int g = (kt * BK + 32 * half) / G;
+            const int g = ((kt0 + kt) * BK + 32 * half) / G - g0;
 #pragma unroll
             for (int j = 0; j < NMAT; ++j) {
                 const uint4 c = *reinterpret_cast<const uint4*>(c_tile + j * kCodeTile + nl * 32 + half * 16);
@@ -351,7 +351,7 @@ int launch_gemm(const CUtensorMap& map, const GemmArgs& a, int E, int max_mblock
 int splits_for(int d, int ff, int G, int mblocks) {
     int splits = choose_splits(d, mblocks);
     while (splits > 1 && (ff / BK) % splits) splits >>= 1;
-    while (splits < 8 && (ff / splits) / G > kMaxGroupsPerCta) splits <<= 1;   // staged-scale capacity
+    while (splits < 8 && (ff / splits) / G + 2 > kMaxGroupsPerCta) splits <<= 1;   // staged-scale capacity
     return splits;
 }
 
