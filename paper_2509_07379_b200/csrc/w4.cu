@@ -118,15 +118,24 @@ __device__ __forceinline__ void stage_x(const __nv_bfloat16* __restrict__ x, int
 // NMAT = 1: row n of W2).  Lane l owns the 32-code chunks c = l + 32 i; the
 // loads for U chunks x NMAT matrices (codes, scale, zero) are issued back to
 // back before any math so each warp keeps U*NMAT*16 B per lane in flight.
-template <int R, int NMAT, int U>
-__device__ __forceinline__ void gemv_row(const W4Ptr (&W)[NMAT], int n, int K, int G,
+// GUARD=false requires (K/32) % (32*U) == 0 (every lane owns exactly
+// nchunks/32 chunks, batches of U) so the batch loop carries no predicates.
+template <int R, int NMAT, int U, int G, bool GUARD>
+__device__ __forceinline__ void gemv_row(const W4Ptr (&W)[NMAT], int n, int K,
                                          const uint32_t* __restrict__ xs, const float* __restrict__ xsum,
                                          float (&acc)[NMAT][R]) {
+    constexpr int CPG_SHIFT = (G == 128) ? 2 : (G == 64 ? 1 : 0);   // log2(chunks per group)
     const int lane = threadIdx.x & 31;
-    const int nchunks = K / 32;
+    const int nchunks = K >> 5;
     const int gpr = K / G;
-    const int cpg = G / 32;                     // chunks per group
-    const size_t row_w = (size_t)K / 8;         // words per row
+    const int zbase = n * gpr;                  // nibble index of group 0 of this row
+    const uint4* crow[NMAT];
+    const uint16_t* srow[NMAT];
+#pragma unroll
+    for (int m = 0; m < NMAT; ++m) {
+        crow[m] = reinterpret_cast<const uint4*>(W[m].codes + (size_t)n * (K >> 3)) + lane;
+        srow[m] = W[m].scales + zbase;
+    }
 #pragma unroll
     for (int m = 0; m < NMAT; ++m)
 #pragma unroll
@@ -135,28 +144,29 @@ __device__ __forceinline__ void gemv_row(const W4Ptr (&W)[NMAT], int n, int K, i
         uint4 cv[U][NMAT];
         uint16_t sv[U][NMAT];
         uint8_t zv[U][NMAT];
+        const int cb = c0 - lane;               // batch base chunk (warp-uniform)
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int c = c0 + 32 * u;
-            if (c < nchunks) {
-                const size_t gi = (size_t)n * gpr + c / cpg;
+            if (!GUARD || c < nchunks) {
+                const int g = c >> CPG_SHIFT;
 #pragma unroll
                 for (int m = 0; m < NMAT; ++m) {
-                    cv[u][m] = ldg_nc_v4(W[m].codes + (size_t)n * row_w + (size_t)c * 4);
-                    sv[u][m] = __ldg(W[m].scales + gi);
-                    zv[u][m] = __ldg(W[m].zeros + (gi >> 1));
+                    cv[u][m] = ldg_nc_v4(crow[m] + cb + 32 * u);
+                    sv[u][m] = __ldg(srow[m] + g);
+                    zv[u][m] = __ldg(W[m].zeros + ((zbase + g) >> 1));
                 }
             }
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int c = c0 + 32 * u;
-            if (c < nchunks) {
-                const size_t gi = (size_t)n * gpr + c / cpg;
+            if (!GUARD || c < nchunks) {
+                const int zsh = ((zbase + (c >> CPG_SHIFT)) & 1) << 2;
                 const int sw = (c >> 1) & 3;
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
-                    const uint32_t* xc = xs + (size_t)r * (K / 2) + c * 16;
+                    const uint32_t* xc = xs + r * (K >> 1) + (c << 4);
                     const float xsm = xsum[r * nchunks + c];
                     uint4 xv[4];
 #pragma unroll
@@ -164,20 +174,20 @@ __device__ __forceinline__ void gemv_row(const W4Ptr (&W)[NMAT], int n, int K, i
 #pragma unroll
                     for (int m = 0; m < NMAT; ++m) {
                         const uint32_t cw[4] = {cv[u][m].x, cv[u][m].y, cv[u][m].z, cv[u][m].w};
-                        float p0 = 0.f, p1 = 0.f;
+                        float p[4] = {0.f, 0.f, 0.f, 0.f};   // 4 independent FHFMA chains
 #pragma unroll
                         for (int i = 0; i < 4; ++i) {
                             const uint32_t xx[4] = {xv[i].x, xv[i].y, xv[i].z, xv[i].w};
 #pragma unroll
                             for (int q = 0; q < 4; ++q) {
                                 const uint32_t pr = nib_pair_magic(cw[i] >> (4 * q));
-                                fma_bf16_lo(p0, pr, xx[q]);
-                                fma_bf16_hi(p1, pr, xx[q]);
+                                fma_bf16_lo(p[(q & 1) * 2], pr, xx[q]);
+                                fma_bf16_hi(p[(q & 1) * 2 + 1], pr, xx[q]);
                             }
                         }
-                        const float z = (float)((zv[u][m] >> ((gi & 1) * 4)) & 15);
+                        const float z = (float)((zv[u][m] >> zsh) & 15);
                         const float sc = __uint_as_float((uint32_t)sv[u][m] << 16);
-                        acc[m][r] = fmaf(sc, (p0 + p1) - (128.f + z) * xsm, acc[m][r]);
+                        acc[m][r] = fmaf(sc, ((p[0] + p[1]) + (p[2] + p[3])) - (128.f + z) * xsm, acc[m][r]);
                     }
                 }
             }
@@ -190,9 +200,9 @@ __device__ __forceinline__ void gemv_row(const W4Ptr (&W)[NMAT], int n, int K, i
 }
 
 // h[r, n] = bf16( silu(x_r . W1[:, n]) * (x_r . W3[:, n]) )
-template <int R>
+template <int R, int G, int U, bool GUARD>
 __global__ void __launch_bounds__(kGemvThreads) swiglu_gemv_kernel(
-    const __nv_bfloat16* __restrict__ x, W4Ptr w1, W4Ptr w3, int K, int N, int G,
+    const __nv_bfloat16* __restrict__ x, W4Ptr w1, W4Ptr w3, int K, int N,
     __nv_bfloat16* __restrict__ h) {
     extern __shared__ __align__(16) uint32_t sm[];
     uint32_t* xs = sm;
@@ -203,7 +213,7 @@ __global__ void __launch_bounds__(kGemvThreads) swiglu_gemv_kernel(
     const W4Ptr W[2] = {w1, w3};
     for (int n = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); n < N; n += warps) {
         float acc[2][R];
-        gemv_row<R, 2, (R == 1 ? 4 : 2)>(W, n, K, G, xs, xsum, acc);
+        gemv_row<R, 2, U, G, GUARD>(W, n, K, xs, xsum, acc);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             if (lane == r) {
@@ -215,9 +225,9 @@ __global__ void __launch_bounds__(kGemvThreads) swiglu_gemv_kernel(
 }
 
 // acc[r, n] += route_w[r] * (h_r . W2[:, n])
-template <int R>
+template <int R, int G, int U, bool GUARD>
 __global__ void __launch_bounds__(kGemvThreads) down_gemv_kernel(
-    const __nv_bfloat16* __restrict__ hin, W4Ptr w2, int K, int N, int G, const float* __restrict__ route_w,
+    const __nv_bfloat16* __restrict__ hin, W4Ptr w2, int K, int N, const float* __restrict__ route_w,
     int route_stride, float* __restrict__ out) {
     extern __shared__ __align__(16) uint32_t sm[];
     uint32_t* xs = sm;
@@ -228,7 +238,7 @@ __global__ void __launch_bounds__(kGemvThreads) down_gemv_kernel(
     const W4Ptr W[1] = {w2};
     for (int n = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); n < N; n += warps) {
         float acc[1][R];
-        gemv_row<R, 1, (R == 1 ? 8 : 4)>(W, n, K, G, xs, xsum, acc);
+        gemv_row<R, 1, U, G, GUARD>(W, n, K, xs, xsum, acc);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             if (lane == r) {
@@ -317,39 +327,77 @@ extern "C" int ds_w4_dequant(const ds_w4_linear* w, int K, int N, int G, void* o
 
 static int check_gemv_shape(int R, int d, int ff, int G) {
     DS_CHECK_ARG(R >= 0 && R <= 64, "w4 gemv: R must be in [0, 64]");
-    DS_CHECK_ARG(d > 0 && ff > 0 && d % 128 == 0 && ff % 128 == 0 && (G == 32 || G == 64 || G == 128),
-                 "w4 gemv: need d, ff multiples of 128 and G in {32,64,128}");
+    DS_CHECK_ARG(d > 0 && ff > 0 && d % 128 == 0 && ff % 128 == 0 && (G == 64 || G == 128),
+                 "w4 gemv: need d, ff multiples of 128 and G in {64,128}");
     return DS_OK;
+}
+
+template <int R, int G, int U, bool GUARD>
+static int swiglu_launch_u(const __nv_bfloat16* x, const ds_w4_expert* e, int d, int ff, __nv_bfloat16* h,
+                           cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(swiglu_gemv_kernel<R, G, U, GUARD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             200 * 1024);
+        attr = true;
+    }
+    const size_t smem = (size_t)R * d * 2 + (size_t)R * (d / 32) * 4;
+    const int grid = gemv_grid((const void*)swiglu_gemv_kernel<R, G, U, GUARD>, smem, ff);
+    swiglu_gemv_kernel<R, G, U, GUARD><<<grid, kGemvThreads, smem, st>>>(x, to_ptr(e->w1), to_ptr(e->w3), d, ff, h);
+    DS_LAUNCH_CHECK("ds_w4_swiglu_gemv");
+    return DS_OK;
+}
+
+template <int R, int G, int U, bool GUARD>
+static int down_launch_u(const __nv_bfloat16* h, const ds_w4_expert* e, int d, int ff, const float* rw, int rs,
+                         float* acc, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(down_gemv_kernel<R, G, U, GUARD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             200 * 1024);
+        attr = true;
+    }
+    const size_t smem = (size_t)R * ff * 2 + (size_t)R * (ff / 32) * 4;
+    const int grid = gemv_grid((const void*)down_gemv_kernel<R, G, U, GUARD>, smem, d);
+    down_gemv_kernel<R, G, U, GUARD><<<grid, kGemvThreads, smem, st>>>(h, to_ptr(e->w2), ff, d, rw, rs, acc);
+    DS_LAUNCH_CHECK("ds_w4_down_gemv");
+    return DS_OK;
+}
+
+// batch size per lane U (16-byte loads in flight per matrix) chosen so that
+// (K/32)/32 is a multiple of U: no predicates in the streaming loop
+template <int R, int G>
+static int swiglu_launch_g(const __nv_bfloat16* x, const ds_w4_expert* e, int d, int ff, __nv_bfloat16* h,
+                           cudaStream_t st) {
+    const int per_lane = (d / 32) % 32 == 0 ? (d / 32) / 32 : 0;
+    if (per_lane && per_lane % 4 == 0) return swiglu_launch_u<R, G, 4, false>(x, e, d, ff, h, st);
+    if (per_lane && per_lane % 3 == 0) return swiglu_launch_u<R, G, 3, false>(x, e, d, ff, h, st);
+    if (per_lane && per_lane % 2 == 0) return swiglu_launch_u<R, G, 2, false>(x, e, d, ff, h, st);
+    return swiglu_launch_u<R, G, 2, true>(x, e, d, ff, h, st);
+}
+
+template <int R, int G>
+static int down_launch_g(const __nv_bfloat16* h, const ds_w4_expert* e, int d, int ff, const float* rw, int rs,
+                         float* acc, cudaStream_t st) {
+    const int per_lane = (ff / 32) % 32 == 0 ? (ff / 32) / 32 : 0;
+    if (per_lane && per_lane % 8 == 0) return down_launch_u<R, G, 8, false>(h, e, d, ff, rw, rs, acc, st);
+    if (per_lane && per_lane % 7 == 0) return down_launch_u<R, G, 7, false>(h, e, d, ff, rw, rs, acc, st);
+    if (per_lane && per_lane % 6 == 0) return down_launch_u<R, G, 6, false>(h, e, d, ff, rw, rs, acc, st);
+    if (per_lane && per_lane % 4 == 0) return down_launch_u<R, G, 4, false>(h, e, d, ff, rw, rs, acc, st);
+    return down_launch_u<R, G, 4, true>(h, e, d, ff, rw, rs, acc, st);
 }
 
 template <int R>
 static int swiglu_launch(const __nv_bfloat16* x, const ds_w4_expert* e, int d, int ff, int G, __nv_bfloat16* h,
                          cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(swiglu_gemv_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
-    }
-    const size_t smem = (size_t)R * d * 2 + (size_t)R * (d / 32) * 4;
-    const int grid = gemv_grid((const void*)swiglu_gemv_kernel<R>, smem, ff);
-    swiglu_gemv_kernel<R><<<grid, kGemvThreads, smem, st>>>(x, to_ptr(e->w1), to_ptr(e->w3), d, ff, G, h);
-    DS_LAUNCH_CHECK("ds_w4_swiglu_gemv");
-    return DS_OK;
+    return G == 128 ? swiglu_launch_g<R, 128>(x, e, d, ff, h, st) : swiglu_launch_g<R, 64>(x, e, d, ff, h, st);
 }
 
 template <int R>
 static int down_launch(const __nv_bfloat16* h, const ds_w4_expert* e, int d, int ff, int G, const float* rw,
                        int rs, float* acc, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(down_gemv_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
-    }
-    const size_t smem = (size_t)R * ff * 2 + (size_t)R * (ff / 32) * 4;
-    const int grid = gemv_grid((const void*)down_gemv_kernel<R>, smem, d);
-    down_gemv_kernel<R><<<grid, kGemvThreads, smem, st>>>(h, to_ptr(e->w2), ff, d, G, rw, rs, acc);
-    DS_LAUNCH_CHECK("ds_w4_down_gemv");
-    return DS_OK;
+    return G == 128 ? down_launch_g<R, 128>(h, e, d, ff, rw, rs, acc, st)
+                    : down_launch_g<R, 64>(h, e, d, ff, rw, rs, acc, st);
 }
 
 extern "C" int ds_w4_swiglu_gemv(const void* x, int R, const ds_w4_expert* e, int d, int ff, int G, void* h,
