@@ -185,9 +185,10 @@ __device__ __forceinline__ void gemv_row(const W4Ptr (&W)[NMAT], int n, int K,
                                 fma_bf16_hi(p[(q & 1) * 2 + 1], pr, xx[q]);
                             }
                         }
-                        const float z = (float)((zv[u][m] >> zsh) & 15);
+                        // 128 + z as an f32 built from bits (no I2F on the XU pipe)
+                        const float z128 = __uint_as_float(0x43000000u | ((((uint32_t)zv[u][m] >> zsh) & 15u) << 16));
                         const float sc = __uint_as_float((uint32_t)sv[u][m] << 16);
-                        acc[m][r] = fmaf(sc, ((p[0] + p[1]) + (p[2] + p[3])) - (128.f + z) * xsm, acc[m][r]);
+                        acc[m][r] = fmaf(sc, ((p[0] + p[1]) + (p[2] + p[3])) - z128 * xsm, acc[m][r]);
                     }
                 }
             }
@@ -201,7 +202,7 @@ __device__ __forceinline__ void gemv_row(const W4Ptr (&W)[NMAT], int n, int K,
 
 // h[r, n] = bf16( silu(x_r . W1[:, n]) * (x_r . W3[:, n]) )
 template <int R, int G, int U, bool GUARD>
-__global__ void __launch_bounds__(kGemvThreads) swiglu_gemv_kernel(
+__global__ void __launch_bounds__(kGemvThreads, 2) swiglu_gemv_kernel(
     const __nv_bfloat16* __restrict__ x, W4Ptr w1, W4Ptr w3, int K, int N,
     __nv_bfloat16* __restrict__ h) {
     extern __shared__ __align__(16) uint32_t sm[];
@@ -226,7 +227,7 @@ __global__ void __launch_bounds__(kGemvThreads) swiglu_gemv_kernel(
 
 // acc[r, n] += route_w[r] * (h_r . W2[:, n])
 template <int R, int G, int U, bool GUARD>
-__global__ void __launch_bounds__(kGemvThreads) down_gemv_kernel(
+__global__ void __launch_bounds__(kGemvThreads, 2) down_gemv_kernel(
     const __nv_bfloat16* __restrict__ hin, W4Ptr w2, int K, int N, const float* __restrict__ route_w,
     int route_stride, float* __restrict__ out) {
     extern __shared__ __align__(16) uint32_t sm[];
