@@ -201,6 +201,12 @@ int ds_link_create(void *copy_stream, size_t chunk_bytes, int depth, ds_link **o
 int ds_link_destroy(ds_link *link);
 int ds_link_submit(ds_link *link, void *dst, const void *src, size_t bytes, void *wait_event,
                    void *done_event, uint64_t *ticket);
+/* Speculative transfer (a predicted prefetch) issued in `chunk_bytes` pieces so a
+ * cancellation leaves little in flight; ds_link_promote switches a confirmed one
+ * back to the link's default chunk size. */
+int ds_link_submit_chunked(ds_link *link, void *dst, const void *src, size_t bytes, size_t chunk_bytes,
+                           void *wait_event, void *done_event, uint64_t *ticket);
+int ds_link_promote(ds_link *link, uint64_t ticket);
 int ds_link_cancel(ds_link *link, uint64_t ticket, size_t *bytes_issued);
 /* Block until every chunk of `ticket` is issued (its done_event recorded) or it was cancelled. */
 int ds_link_wait_issued(ds_link *link, uint64_t ticket);

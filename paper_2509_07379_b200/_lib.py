@@ -85,6 +85,8 @@ _SIGS = {
     "ds_link_destroy": (_I, [_P]),
     "ds_link_submit": (_I, [_P, _P, _P, _SZ, _P, _P, C.POINTER(C.c_uint64)]),
     "ds_link_cancel": (_I, [_P, C.c_uint64, C.POINTER(_SZ)]),
+    "ds_link_submit_chunked": (_I, [_P, _P, _P, _SZ, _SZ, _P, _P, C.POINTER(C.c_uint64)]),
+    "ds_link_promote": (_I, [_P, C.c_uint64]),
     "ds_link_wait_issued": (_I, [_P, C.c_uint64]),
     "ds_link_idle": (_I, [_P]),
     "ds_link_stats": (_I, [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),

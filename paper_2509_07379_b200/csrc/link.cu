@@ -35,6 +35,7 @@ struct Xfer {
     const char* src;
     size_t bytes;
     size_t next = 0;        // bytes already issued
+    size_t chunk = 0;       // chunk size of this transfer (speculative transfers use small chunks)
     cudaEvent_t wait_ev;
     cudaEvent_t done_ev;
     bool cancelled = false;
@@ -86,7 +87,7 @@ void issue_locked(ds_link* L) {
     while (!L->pending.empty() && (int)L->inflight.size() < L->depth) {
         auto x = L->pending.front();
         if (x->next == 0 && x->wait_ev) cudaStreamWaitEvent(L->stream, x->wait_ev, 0);
-        const size_t n = std::min(L->chunk, x->bytes - x->next);
+        const size_t n = std::min(x->chunk ? x->chunk : L->chunk, x->bytes - x->next);
         cudaError_t e = cudaMemcpyAsync(x->dst + x->next, x->src + x->next, n, cudaMemcpyHostToDevice, L->stream);
         if (e != cudaSuccess) L->error = (int)e;
         cudaEvent_t ev = take_event(L);
@@ -174,6 +175,38 @@ extern "C" int ds_link_submit(ds_link* L, void* dst, const void* src, size_t byt
         issue_locked(L);
     }
     L->cv.notify_one();
+    return DS_OK;
+}
+
+extern "C" int ds_link_submit_chunked(ds_link* L, void* dst, const void* src, size_t bytes, size_t chunk_bytes,
+                                      void* wait_event, void* done_event, uint64_t* ticket) {
+    DS_CHECK_ARG(L && dst && src && bytes > 0 && ticket && chunk_bytes >= 4096, "ds_link_submit_chunked: bad arguments");
+    auto x = std::make_shared<Xfer>();
+    x->dst = static_cast<char*>(dst);
+    x->src = static_cast<const char*>(src);
+    x->bytes = bytes;
+    x->chunk = chunk_bytes;
+    x->wait_ev = static_cast<cudaEvent_t>(wait_event);
+    x->done_ev = static_cast<cudaEvent_t>(done_event);
+    {
+        std::lock_guard<std::mutex> g(L->mu);
+        x->ticket = L->next_ticket++;
+        L->pending.push_back(x);
+        L->live[x->ticket] = x;
+        *ticket = x->ticket;
+        issue_locked(L);
+    }
+    L->cv.notify_one();
+    return DS_OK;
+}
+
+// A speculative transfer the gate confirmed: finish it with the link's
+// default (large) chunks.
+extern "C" int ds_link_promote(ds_link* L, uint64_t ticket) {
+    DS_CHECK_ARG(L, "ds_link_promote: NULL link");
+    std::lock_guard<std::mutex> g(L->mu);
+    auto it = L->live.find(ticket);
+    if (it != L->live.end()) it->second->chunk = 0;
     return DS_OK;
 }
 

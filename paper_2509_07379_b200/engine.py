@@ -153,6 +153,7 @@ class LinkQueue:
         self.chunk = blob if chunk_bytes <= 0 else min(chunk_bytes, blob)
         self.depth = depth
         self.cancel_enabled = cancel
+        self.spec_chunk = min(self.chunk, 2 << 20)
         h = C.c_void_p()
         _lib.call("ds_link_create", C.c_void_p(cache.copy_stream.cuda_stream), self.chunk, depth, C.byref(h))
         self.handle = h
@@ -168,17 +169,28 @@ class LinkQueue:
         except Exception:
             pass
 
-    def submit(self, slot: int, layer: int, expert: int) -> Transfer:
+    def submit(self, slot: int, layer: int, expert: int, speculative: bool = False) -> Transfer:
+        """Queue expert (layer, expert) into slot.  Speculative (predicted)
+        transfers use small chunks until promote(), so cancelling leaves at
+        most `depth` small chunks in flight."""
         c = self.cache
         C = self.C
         t = C.c_uint64()
         wait = C.c_void_p(c.free[slot].cuda_event) if c.used[slot] else None
-        self.lib.call("ds_link_submit", self.handle, C.c_void_p(c.slots[slot].data_ptr()),
-                      C.c_void_p(c.store.blob(layer, expert).data_ptr()), c.store.blob_bytes, wait,
-                      C.c_void_p(c.ready[slot].cuda_event), C.byref(t))
+        args = (self.handle, C.c_void_p(c.slots[slot].data_ptr()), C.c_void_p(c.store.blob(layer, expert).data_ptr()),
+                c.store.blob_bytes)
+        if speculative and self.cancel_enabled and self.spec_chunk < self.chunk:
+            self.lib.call("ds_link_submit_chunked", *args, self.spec_chunk, wait, C.c_void_p(c.ready[slot].cuda_event),
+                          C.byref(t))
+        else:
+            self.lib.call("ds_link_submit", *args, wait, C.c_void_p(c.ready[slot].cuda_event), C.byref(t))
         c.content[slot] = (layer, expert)
         c.n_copies += 1
         return Transfer(slot, layer, expert, t.value)
+
+    def promote(self, tr: Transfer) -> None:
+        if self.cancel_enabled:
+            self.lib.call("ds_link_promote", self.handle, tr.ticket)
 
     def cancel(self, tr: Transfer) -> None:
         if not self.cancel_enabled:
@@ -592,6 +604,7 @@ class Engine:
                     continue
                 if p in E:
                     slot_of[p], trs[p] = pending[p]
+                    link.promote(trs[p])                       # confirmed: finish with large chunks
                 else:
                     link.cancel(pending[p][1])                 # drop its not-yet-issued chunks
             used = set(slot_of.values())
@@ -625,7 +638,7 @@ class Engine:
             free = [s_ for s_ in range(self.n_slots) if s_ not in cur][: self.k]
             pending = {}
             for e, s_ in zip([e for e in order if e in self.owned_set], free):
-                pending[e] = (s_, link.submit(s_, l + 1, e))
+                pending[e] = (s_, link.submit(s_, l + 1, e, speculative=True))
             self._pred_next = (Pn, order, pending)
         return out, E
 
