@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="mixtral-8x7b")
-    ap.add_argument("--policy", default="duoserve", choices=["duoserve", "oracle", "ondemand"])
+    ap.add_argument("--policy", default="duoserve", choices=["duoserve", "oracle", "ondemand", "prefetchall"])
     ap.add_argument("--prefill", type=int, default=512)
     ap.add_argument("--decode", type=int, default=128)
     ap.add_argument("--warmup-decode", type=int, default=None,
@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--chunk-mb", type=float, default=8.0)
     ap.add_argument("--link-depth", type=int, default=2)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--ep", action="store_true",
+                    help="under torchrun: expert parallelism (rank r owns experts e %% N == r, per-rank pinned "
+                         "shard + cache, NCCL all-reduce combine) on ONE request instead of N replicas")
     ap.add_argument("--out", default=None, help="also write the JSON line to this file")
     return ap.parse_args()
 
@@ -250,11 +253,16 @@ def run_ours(args):
     shape = load_shape(args.config)
     t_setup = time.time()
     net, pop, aff = predictor_inputs(shape) if args.policy == "duoserve" else (None, None, None)
+    ep = None
+    if args.ep and ws > 1:
+        from paper_2509_07379_b200.ep import EPConfig
+        ep = EPConfig(rank, ws)
     eng = Engine(shape, args.policy if args.policy != "oracle" else "duoserve", seed=args.seed, device=dev,
                  predictor=net, pop=pop, aff=aff, max_seq=args.prefill + args.decode + 8,
                  max_prefill=args.prefill, cancel_mispredicted=not args.no_cancel, chunk_mb=args.chunk_mb,
-                 link_depth=args.link_depth)
-    gen = torch.Generator().manual_seed(args.seed + 1000 * rank)
+                 link_depth=args.link_depth, ep=ep)
+    # replicas: an independent request per rank; EP: every rank serves the same request
+    gen = torch.Generator().manual_seed(args.seed + (0 if ep else 1000 * rank))
     ids_host = torch.randint(0, shape.vocab, (args.prefill,), generator=gen).pin_memory()
     if args.policy == "oracle":
         # record the routing once, then replay it as the perfect predictor (SPEC DuoServeOracle)
@@ -262,7 +270,7 @@ def run_ours(args):
         eng.generate(ids_host, args.decode + 1)
         paths = eng.paths_decode
         eng = Engine(shape, "oracle", seed=args.seed, device=dev, dense=eng.W, store=eng.store,
-                     oracle_paths=paths, max_seq=args.prefill + args.decode + 8, max_prefill=args.prefill,
+                     oracle_paths=paths, ep=ep, max_seq=args.prefill + args.decode + 8, max_prefill=args.prefill,
                      cancel_mispredicted=not args.no_cancel, chunk_mb=args.chunk_mb, link_depth=args.link_depth)
     setup_s = time.time() - t_setup
     prof = eng.enable_profile()
@@ -308,6 +316,14 @@ def run_ours(args):
     torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
+    # one extra, untimed step with the device timeline on (per-chunk timing
+    # events): link busy fraction and copy/compute overlap fraction
+    n_spans = {n: len(v) for n, v in prof.spans.items()}     # the roofline uses the timed steps only
+    tl = eng.enable_timeline()
+    eng.reset()
+    tl.begin()
+    timeline_bytes = one_step(args.decode)["h2d_experts"]
+    timeline = tl.end()
     ms_step = statistics.median(r["ttft_ms"] + r["decode_ms"] for r in res)
     e2e_ms = statistics.median(r["e2e_wall_ms"] for r in res)
     if ws > 1:
@@ -322,19 +338,21 @@ def run_ours(args):
     peaks = measured_peaks()
     link_gbs = eng.link_peak_gbs()
     h2d_step = r0["h2d_experts"] + args.prefill * 8
+    prof.spans = {n: v[:n_spans[n]] for n, v in prof.spans.items() if n in n_spans}
     kern = prof.summary(peaks)
     res_b = eng.resident_bytes()
     peak_dev = torch.cuda.max_memory_allocated(dev)
     line = {
         "metric": METRIC, "value": round(ms_step, 1), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms_step, 1), "higher_is_better": False, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 1), "higher_is_better": False,
+        "scaling": "strong" if ep else "weak",
         "vs_baseline": None, "dtype": "bf16 activations, W4 (int4 g128) experts, f32 accumulate",
         "data": "synthetic (random-init W4 experts from a counter-based generator, random prompt ids)",
         "config": {"workload": f"{shape.name}-shaped W4, batch 1, prefill {args.prefill} + decode {args.decode}, "
                                f"1 request per GPU, policy {args.policy}"
                                f"{'' if args.no_cancel else ' + chunked cancellable prefetch'}",
-                   "model": shape.name, "global_batch": ws, "seq_len": args.prefill + args.decode,
-                   "parallelism": f"replicas{ws}" if ws > 1 else "single-gpu",
+                   "model": shape.name, "global_batch": 1 if ep else ws, "seq_len": args.prefill + args.decode,
+                   "parallelism": (f"ep{ws}" if ep else f"replicas{ws}") if ws > 1 else "single-gpu",
                    "expert_slots": eng.n_slots,
                    "l2": "inputs > L2: every expert byte is streamed from pinned host memory per request"},
         "ttft_ms": round(ttft, 2), "decode_tok_s": round(args.decode / (dec_ms / 1e3), 3),
@@ -346,7 +364,10 @@ def run_ours(args):
                  "peak_gbs_measured": round(link_gbs, 2),
                  "frac": round(r0["h2d_experts"] / ((ttft + dec_ms) / 1e3) / 1e9 / link_gbs, 3),
                  "ttft_floor_ms": round(eng.prefill_bytes_floor() / link_gbs / 1e6, 1),
-                 "decode_floor_ms_per_token": round(eng.decode_bytes_floor() / link_gbs / 1e6, 2)},
+                 "decode_floor_ms_per_token": round(eng.decode_bytes_floor() / link_gbs / 1e6, 2),
+                 "timeline": {k: (round(v, 4) if isinstance(v, float) else v) for k, v in timeline.items()},
+                 "busy_gbs": round(timeline_bytes / (timeline["copy_busy_ms"] / 1e3) / 1e9, 2)
+                 if timeline["copy_busy_ms"] else None},
         "roofline": kern["dominant"],
         "kernels": kern["all"],
         "gpu_launches": kern["launches"],

@@ -213,6 +213,14 @@ int ds_link_wait_issued(ds_link *link, uint64_t ticket);
 int ds_link_idle(ds_link *link);
 int ds_link_stats(ds_link *link, uint64_t *bytes_issued, uint64_t *bytes_wasted, uint64_t *chunks);
 int ds_link_reset_stats(ds_link *link);
+/* Trace mode (measurement only): a timing event pair around every chunk.
+ * ds_link_trace_read returns the copy-busy intervals [start_ms, end_ms] of the
+ * chunks issued since the last read, relative to `ref_event` (a timing
+ * cudaEvent_t recorded earlier on the same device), for the copy/compute
+ * overlap fraction. */
+int ds_link_trace(ds_link *link, int enable);
+int ds_link_trace_read(ds_link *link, void *ref_event, float *start_ms, float *end_ms, size_t max_spans,
+                       size_t *n_out);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -18,6 +18,9 @@ Two parts:
         each miss is re-fetched (blocking); prefetch_hits + prefetch_misses
         = k*(L-1) per token.
       * ondemand: fetch E after the gate every layer (prefill: A_l).
+      * prefetchall (MoESys baseline): every layer visit
+        transfers all M experts (ascending) into one of two banks of M slots
+        (2M = slot_count), eagerly and in visit order, whatever the gate says.
  2. timeline_*: integer-nanosecond event model used to pin the SPEC's
     hand-traced fixtures (32/48/40 ms prefill, 20/30/25 ms
     decode).  Interpretation of sync point 2 with 2k slots: the next layer's
@@ -33,10 +36,11 @@ def _sorted(x):
     return [int(e) for e in sorted(x)]
 
 
-def cache_log_prefill(E_by_token, L: int, policy: str = "duoserve", owned=None):
+def cache_log_prefill(E_by_token, L: int, policy: str = "duoserve", owned=None, M: int = 8):
     """E_by_token: list over prefill tokens of L-tuples of selections.
     owned: expert ids of this rank under expert parallelism (None = all);
-    the speculative first transfer is then the rank's lowest owned expert."""
+    the speculative first transfer is then the rank's lowest owned expert.
+    M: experts per layer (used by prefetchall only)."""
     log = []
     for l in range(L):
         A = set()
@@ -49,17 +53,18 @@ def cache_log_prefill(E_by_token, L: int, policy: str = "duoserve", owned=None):
         elif policy == "ondemand":
             fetch = _sorted(mine)
         elif policy == "prefetchall":
-            fetch = list(range(max(max(A) + 1, 0)))  # caller passes M via prefetchall_M
+            fetch = list(range(M)) if owned is None else _sorted(owned)
         else:
             raise ValueError(policy)
         log.append({"phase": "prefill", "layer": l, "fetch": fetch, "activated": _sorted(A)})
     return log
 
 
-def cache_log_decode(paths, preds, L: int, policy: str = "duoserve", owned=None):
+def cache_log_decode(paths, preds, L: int, policy: str = "duoserve", owned=None, M: int = 8):
     """paths[t][l] = gate selection of decode token t at layer l;
-    preds[t][l] = predicted set for l >= 1 (ignored for ondemand).
-    owned: expert ids of this rank under expert parallelism (None = all)."""
+    preds[t][l] = predicted set for l >= 1 (ignored for ondemand/prefetchall).
+    owned: expert ids of this rank under expert parallelism (None = all).
+    M: experts per layer (used by prefetchall only)."""
     own = None if owned is None else set(owned)
     keep = (lambda xs: _sorted(xs)) if own is None else (lambda xs: _sorted(set(xs) & own))
     log = []
@@ -67,6 +72,10 @@ def cache_log_decode(paths, preds, L: int, policy: str = "duoserve", owned=None)
     for t, path in enumerate(paths):
         for l in range(L):
             E = _sorted(path[l])
+            if policy == "prefetchall":
+                log.append({"phase": "decode", "token": t, "layer": l,
+                            "fetch": list(range(M)) if own is None else _sorted(own), "kind": "prefetchall"})
+                continue
             if l == 0 or policy == "ondemand":
                 log.append({"phase": "decode", "token": t, "layer": l, "fetch": keep(E), "kind": "ondemand"})
                 continue

@@ -91,6 +91,8 @@ _SIGS = {
     "ds_link_idle": (_I, [_P]),
     "ds_link_stats": (_I, [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "ds_link_reset_stats": (_I, [_P]),
+    "ds_link_trace": (_I, [_P, _I]),
+    "ds_link_trace_read": (_I, [_P, _P, C.POINTER(C.c_float), C.POINTER(C.c_float), _SZ, C.POINTER(_SZ)]),
     "ds_w4_grouped_ffn": (_I, [_P, C.POINTER(_I), _I, C.POINTER(W4Expert), _I, _I, _I, _P, _P, _P, _SZ, _P]),
 }
 

@@ -59,6 +59,11 @@ struct ds_link {
     std::vector<cudaEvent_t> pool;
     uint64_t next_ticket = 1;
     uint64_t bytes_issued = 0, bytes_wasted = 0, chunks = 0;
+    // trace mode: a timing event pair around every chunk (copy-busy intervals
+    // for the copy/compute overlap fraction); off by default
+    bool trace = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> spans;
+    std::vector<cudaEvent_t> tpool;
     int error = 0;
     bool stop = false;
     std::thread worker;
@@ -78,6 +83,17 @@ cudaEvent_t take_event(ds_link* L) {
     return e;
 }
 
+cudaEvent_t take_timing_event(ds_link* L) {
+    if (!L->tpool.empty()) {
+        cudaEvent_t e = L->tpool.back();
+        L->tpool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
 // Issue as many chunks as the depth allows.  Called with L->mu held.
 void issue_locked(ds_link* L) {
     while (!L->inflight.empty() && cudaEventQuery(L->inflight.front()) == cudaSuccess) {
@@ -88,8 +104,18 @@ void issue_locked(ds_link* L) {
         auto x = L->pending.front();
         if (x->next == 0 && x->wait_ev) cudaStreamWaitEvent(L->stream, x->wait_ev, 0);
         const size_t n = std::min(x->chunk ? x->chunk : L->chunk, x->bytes - x->next);
+        cudaEvent_t t0 = nullptr, t1 = nullptr;
+        if (L->trace) {
+            t0 = take_timing_event(L);
+            t1 = take_timing_event(L);
+            cudaEventRecord(t0, L->stream);
+        }
         cudaError_t e = cudaMemcpyAsync(x->dst + x->next, x->src + x->next, n, cudaMemcpyHostToDevice, L->stream);
         if (e != cudaSuccess) L->error = (int)e;
+        if (L->trace) {
+            cudaEventRecord(t1, L->stream);
+            L->spans.emplace_back(t0, t1);
+        }
         cudaEvent_t ev = take_event(L);
         cudaEventRecord(ev, L->stream);
         L->inflight.push_back(ev);
@@ -153,6 +179,11 @@ extern "C" int ds_link_destroy(ds_link* L) {
     cudaStreamSynchronize(L->stream);
     for (auto e : L->inflight) cudaEventDestroy(e);
     for (auto e : L->pool) cudaEventDestroy(e);
+    for (auto& sp : L->spans) {
+        cudaEventDestroy(sp.first);
+        cudaEventDestroy(sp.second);
+    }
+    for (auto e : L->tpool) cudaEventDestroy(e);
     delete L;
     return DS_OK;
 }
@@ -260,5 +291,43 @@ extern "C" int ds_link_reset_stats(ds_link* L) {
     DS_CHECK_ARG(L, "ds_link_reset_stats: NULL link");
     std::lock_guard<std::mutex> g(L->mu);
     L->bytes_issued = L->bytes_wasted = L->chunks = 0;
+    return DS_OK;
+}
+
+extern "C" int ds_link_trace(ds_link* L, int enable) {
+    DS_CHECK_ARG(L, "ds_link_trace: NULL link");
+    std::lock_guard<std::mutex> g(L->mu);
+    L->trace = enable != 0;
+    return DS_OK;
+}
+
+// Copy-busy intervals of the chunks issued since the last read, in ms relative
+// to `ref_event` (a timing event recorded before them on any stream of the
+// device).  Synchronises on the last chunk; returns the spans' events to the
+// pool.  *n_out = number of spans written (<= max_spans; the rest are dropped).
+extern "C" int ds_link_trace_read(ds_link* L, void* ref_event, float* start_ms, float* end_ms, size_t max_spans,
+                                  size_t* n_out) {
+    DS_CHECK_ARG(L && ref_event && n_out, "ds_link_trace_read: bad arguments");
+    std::lock_guard<std::mutex> g(L->mu);
+    cudaEvent_t ref = static_cast<cudaEvent_t>(ref_event);
+    size_t n = 0;
+    int err = 0;
+    if (!L->spans.empty()) cudaEventSynchronize(L->spans.back().second);
+    for (auto& sp : L->spans) {
+        if (n < max_spans && start_ms && end_ms) {
+            float a = 0.f, b = 0.f;
+            cudaError_t e1 = cudaEventElapsedTime(&a, ref, sp.first);
+            cudaError_t e2 = cudaEventElapsedTime(&b, ref, sp.second);
+            if (e1 != cudaSuccess || e2 != cudaSuccess) err = (int)(e1 != cudaSuccess ? e1 : e2);
+            start_ms[n] = a;
+            end_ms[n] = b;
+            ++n;
+        }
+        L->tpool.push_back(sp.first);
+        L->tpool.push_back(sp.second);
+    }
+    L->spans.clear();
+    *n_out = n;
+    if (err) return fail(err, "ds_link_trace_read: cudaEventElapsedTime failed: %s", cudaGetErrorString((cudaError_t)err));
     return DS_OK;
 }

@@ -27,7 +27,10 @@ Schedules (policy "duoserve"):
       device history buffer; sync point 2 issues the prefetch of P_{l+1} into
       the two slots released by layer l-1.
 Policy "oracle" replays a recorded routing as the prediction (the SPEC's
-DuoServeOracle); "ondemand" fetches after the gate (ACC baseline).
+DuoServeOracle); "ondemand" fetches after the gate (ACC baseline);
+"prefetchall" (MoESys baseline) streams all M experts of
+every layer visit into one of two banks of M slots, the next visit's bank
+filling while the current one computes.
 """
 
 from __future__ import annotations
@@ -96,6 +99,7 @@ class ExpertCache:
         self.content = [None] * n_slots          # (layer, expert) resident or in flight
         self.bytes_copied = 0
         self.n_copies = 0
+        self.trace = None                        # list of (ev0, ev1) timing pairs when tracing
         sh = store.shape
         self._structs = [ops.expert_struct(self.slots[i].data_ptr(), sh.hidden, sh.ffn, sh.group_size)
                          for i in range(n_slots)]
@@ -109,7 +113,13 @@ class ExpertCache:
         with torch.cuda.stream(self.copy_stream):
             if self.used[slot]:
                 self.copy_stream.wait_event(self.free[slot])
+            if self.trace is not None:
+                t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                t0.record(self.copy_stream)
             self.slots[slot].copy_(self.store.blob(layer, expert), non_blocking=True)
+            if self.trace is not None:
+                t1.record(self.copy_stream)
+                self.trace.append((t0, t1))
             self.ready[slot].record(self.copy_stream)
         self.content[slot] = (layer, expert)
         self.bytes_copied += self.store.blob_bytes
@@ -213,6 +223,17 @@ class LinkQueue:
 
     def reset_stats(self) -> None:
         self.lib.call("ds_link_reset_stats", self.handle)
+
+    def set_trace(self, on: bool) -> None:
+        self.lib.call("ds_link_trace", self.handle, int(on))
+
+    def trace_read(self, ref_event) -> list:
+        """Copy-busy (start, end) ms of the chunks issued since the last read, relative to ref_event."""
+        C = self.C
+        cap = 1 << 20
+        a, b, n = (C.c_float * cap)(), (C.c_float * cap)(), C.c_size_t()
+        self.lib.call("ds_link_trace_read", self.handle, C.c_void_p(ref_event.cuda_event), a, b, cap, C.byref(n))
+        return [(a[i], b[i]) for i in range(n.value)]
 
     def set_chunk(self, chunk_bytes: int) -> None:
         """Recreate the native link with a new chunk size (idle link only)."""
@@ -324,8 +345,6 @@ class Engine:
             if oracle_paths is None:
                 raise ValueError("policy 'oracle' needs the recorded decode routing (oracle_paths)")
             self.driver = TraceDriver(oracle_paths)
-        elif self.policy is SchedulerPolicy.PREFETCH_ALL:
-            raise NotImplementedError("prefetchall policy is not implemented on the B200 runtime yet")
         dev = self.device
         # decode buffers
         self.hist = torch.zeros((1, self.L * self.k), dtype=torch.int32, device=dev)
@@ -375,6 +394,8 @@ class Engine:
         self._spec = None                     # (slot, layer, expert) speculative prefill fetch
         self._ring = 0
         self._pred_next = None
+        self._pa_v = 0                        # prefetchall: layer visits computed so far
+        self._pa_queued = 0                   # prefetchall: layer visits queued on the copy stream
         self.hist.zero_()
         self.d2h_bytes = 0
         if hasattr(self, "link"):
@@ -391,7 +412,10 @@ class Engine:
         T = ids.numel()
         h = self.W.embed[ids]
         idx_all = []
-        self._spec_fetch(0)
+        if self.policy is SchedulerPolicy.PREFETCH_ALL:
+            self._pa_fill(self._pa_v + 2)
+        else:
+            self._spec_fetch(0)
         for l in range(self.L):
             h = attention_block(self.shape, self.W.layers[l], h, self.kv, l, 0, self.cos, self.sin)
             h, idx_host = self._moe_prefill(l, h, T)
@@ -491,9 +515,31 @@ class Engine:
         self._ring = (self._ring + 1) % self.n_slots
         return s
 
+    # ---------------------------------------------------------- prefetchall
+    def _pa_slot(self, v: int, e: int) -> int:
+        """Bank v % 2 of M slots, one per (owned) expert."""
+        return (v % 2) * len(self.owned) + self.store.local[e]
+
+    def _pa_fill(self, upto: int) -> None:
+        """Queue every owned expert of the layer visits [queued, upto) (visit v
+        is layer v % L: prefill layers then each decode token's layers)."""
+        while self._pa_queued < upto:
+            v = self._pa_queued
+            for e in self.owned:
+                self.cache.load(self._pa_slot(v, e), v % self.L, e)
+            self._pa_queued += 1
+
+    def _pa_done(self) -> None:
+        """The current visit's compute is queued: free its bank and stream the visit after next into it."""
+        v = self._pa_v
+        for e in self.owned:
+            self.cache.release(self._pa_slot(v, e))
+        self._pa_v += 1
+        self._pa_fill(self._pa_v + 2)
+
     def _spec_fetch(self, layer: int) -> None:
         """Speculative first transfer of layer `layer` (expert 0) to overlap attention."""
-        if layer >= self.L or self.policy is SchedulerPolicy.ON_DEMAND:
+        if layer >= self.L or self.policy in (SchedulerPolicy.ON_DEMAND, SchedulerPolicy.PREFETCH_ALL):
             self._spec = None
             return
         slot = self._next_ring_slot()
@@ -521,6 +567,8 @@ class Engine:
         A_all = [e for e in range(self.M) if off[e + 1] > off[e]]
         A = [e for e in A_all if e in self.owned_set]       # this rank's share (all on one GPU)
         plan = []                                           # (expert, slot, already_queued)
+        if self.policy is SchedulerPolicy.PREFETCH_ALL:
+            return self._moe_prefill_all(l, h, T, A, A_all, off, w, idx, idx_host)
         if self.policy is SchedulerPolicy.ON_DEMAND:
             plan = [(e, i % self.n_slots, False) for i, e in enumerate(A)]
         else:
@@ -538,14 +586,7 @@ class Engine:
                 self.cache.load(slot, l, e)
         for i, (e, slot, _) in enumerate(plan):
             if off[e + 1] > off[e]:
-                st = self.cache.acquire(slot)
-                lo, hi = off[e], off[e + 1]
-                ev = self.prof.start() if self.prof else None
-                ops.grouped_ffn(self.p_xperm[lo:hi], [0, hi - lo], [st], self.d, self.ff, self.G,
-                                self.p_h[lo:hi], self.p_y[lo:hi], self.p_ws)
-                if self.prof:
-                    self.prof.stop("K3 w4_grouped_ffn (tcgen05)", ev, self.store.blob_bytes,
-                                   6.0 * (hi - lo) * self.d * self.ff)
+                self._prefill_ffn(e, slot, off)
             self.cache.release(slot)
             if i + window < len(plan):
                 e2, slot2, queued2 = plan[i + window]
@@ -553,6 +594,19 @@ class Engine:
                     self.cache.load(slot2, l, e2)
         # next layer's first expert streams while this layer combines + next attention runs
         self._spec_fetch(l + 1)
+        return self._prefill_combine(h, T, w, idx), idx_host.numpy()
+
+    def _prefill_ffn(self, e: int, slot: int, off) -> None:
+        lo, hi = off[e], off[e + 1]
+        st = self.cache.acquire(slot)
+        ev = self.prof.start() if self.prof else None
+        ops.grouped_ffn(self.p_xperm[lo:hi], [0, hi - lo], [st], self.d, self.ff, self.G,
+                        self.p_h[lo:hi], self.p_y[lo:hi], self.p_ws)
+        if self.prof:
+            self.prof.stop("K3 w4_grouped_ffn (tcgen05)", ev, self.store.blob_bytes,
+                           6.0 * (hi - lo) * self.d * self.ff)
+
+    def _prefill_combine(self, h, T, w, idx):
         out = torch.empty_like(h)
         if self.ep is None:
             ops.unpermute_combine(self.p_y[:T * self.k], self.p_pos[:T * self.k], w, h, out)
@@ -561,7 +615,15 @@ class Engine:
             ops.unpermute_partial(self.p_y[:T * self.k], self.p_pos[:T * self.k], w, idx, self.owner_bits, part)
             self.ep.all_reduce_(part)                       # sum of the ranks' expert terms
             ops.combine_finalize(part, h, out)
-        return out, idx_host.numpy()
+        return out
+
+    def _moe_prefill_all(self, l, h, T, A, A_all, off, w, idx, idx_host):
+        """prefetchall: the whole layer was queued two visits ago; compute the activated experts."""
+        self.log.append({"phase": "prefill", "layer": l, "fetch": list(self.owned), "activated": A_all})
+        for e in A:
+            self._prefill_ffn(e, self._pa_slot(self._pa_v, e), off)
+        self._pa_done()
+        return self._prefill_combine(h, T, w, idx), idx_host.numpy()
 
     # --------------------------------------------------------------- decode
     def _moe_decode(self, l: int, h: torch.Tensor, pre: torch.Tensor | None = None, out: torch.Tensor | None = None):
@@ -587,6 +649,13 @@ class Engine:
         slot_of, trs = {}, {}
         miss = []
         mine = [e for e in E if e in self.owned_set]
+        if self.policy is SchedulerPolicy.PREFETCH_ALL:
+            self.log.append({"phase": "decode", "token": self.t_decode, "layer": l, "fetch": list(self.owned),
+                             "kind": "prefetchall"})
+            for e in mine:
+                self._decode_ffn(a, self.cache.acquire(self._pa_slot(self._pa_v, e)), E.index(e))
+            self._pa_done()
+            return self._decode_combine(h, out), E
         if l == 0 or not use_pred:
             base = 0 if (l % 2 == 0 or self.n_slots < 2 * self.k) else self.k
             for j, e in enumerate(mine):
@@ -619,18 +688,9 @@ class Engine:
         for e in [x for x in mine if x not in miss] + miss:
             j = E.index(e)
             link.flush(trs[e])
-            st = self.cache.acquire(slot_of[e])
-            ev = self.prof.start() if self.prof else None
-            ops.swiglu_gemv(a, st, self.d, self.ff, self.G, self.h_buf)
-            ops.down_gemv(self.h_buf, st, self.d, self.ff, self.G, self.w1[0, j:], 1, self.acc)
-            if self.prof:
-                self.prof.stop("K4 w4_swiglu_gemv+down_gemv", ev, self.store.blob_bytes)
+            self._decode_ffn(a, self.cache.acquire(slot_of[e]), j)
             self.cache.release(slot_of[e])
-        if out is None:
-            out = torch.empty_like(h)
-        if self.ep is not None:
-            self.ep.all_reduce_(self.acc)                      # sum of the ranks' expert terms
-        ops.combine_finalize(self.acc, h, out)
+        out = self._decode_combine(h, out)
         # sync point 2: prediction for l+1 ready -> prefetch into the slots layer l-1 used
         if use_pred and l + 1 < self.L:
             Pn, order = self.driver.result(link)
@@ -641,6 +701,22 @@ class Engine:
                 pending[e] = (s_, link.submit(s_, l + 1, e, speculative=True))
             self._pred_next = (Pn, order, pending)
         return out, E
+
+    def _decode_ffn(self, a, st, j: int) -> None:
+        """K4: acc += w_j * W2 (silu(a W1) * (a W3)) for the expert in slot struct st."""
+        ev = self.prof.start() if self.prof else None
+        ops.swiglu_gemv(a, st, self.d, self.ff, self.G, self.h_buf)
+        ops.down_gemv(self.h_buf, st, self.d, self.ff, self.G, self.w1[0, j:], 1, self.acc)
+        if self.prof:
+            self.prof.stop("K4 w4_swiglu_gemv+down_gemv", ev, self.store.blob_bytes)
+
+    def _decode_combine(self, h, out):
+        if out is None:
+            out = torch.empty_like(h)
+        if self.ep is not None:
+            self.ep.all_reduce_(self.acc)                      # sum of the ranks' expert terms
+        ops.combine_finalize(self.acc, h, out)
+        return out
 
     # -------------------------------------------------------------- metrics
     def link_peak_gbs(self) -> float:
@@ -661,6 +737,12 @@ class Engine:
             self._link_peak = 16 * src.numel() / (e0.elapsed_time(e1) / 1e3) / 1e9
             self.cache.used[0] = False
         return self._link_peak
+
+    def enable_timeline(self) -> "Timeline":
+        """Device timeline of copy-busy intervals and expert-FFN spans (needs enable_profile())."""
+        if self.prof is None:
+            self.enable_profile()
+        return Timeline(self)
 
     def h2d_bytes(self) -> int:
         """Expert bytes moved host->device so far (prefill copies + decode link chunks)."""
@@ -692,6 +774,63 @@ class Engine:
         pred = self.driver.nbytes if isinstance(self.driver, MLPDriver) else 0
         return {"non_moe": self.W.nbytes(), "expert_slots": self.cache.nbytes, "predictor": pred,
                 "kv_cache": self.kv.nbytes, "model_total": self.shape.total_bytes}
+
+
+def _union(iv: list) -> list:
+    out = []
+    for a, b in sorted(iv):
+        if out and a <= out[-1][1]:
+            out[-1][1] = max(out[-1][1], b)
+        else:
+            out.append([a, b])
+    return out
+
+
+def _covered(a: float, b: float, union: list) -> float:
+    return sum(max(0.0, min(b, y) - max(a, x)) for x, y in union)
+
+
+class Timeline:
+    """Per-step device timeline (CUDA timing events, common reference event):
+    copy-busy intervals of every expert transfer (ExpertCache copies and the
+    native link's chunks, csrc/link.cu trace mode) and the expert-FFN spans
+    (K3/K4, from the KernelProfiler).  Reports the link busy fraction, the
+    achieved GB/s while busy and the copy/compute overlap fraction =
+    (expert compute time that runs while a transfer is in flight) / (total
+    expert compute time) — SURVEY.md §8d."""
+
+    def __init__(self, eng: "Engine"):
+        self.eng = eng
+        eng.cache.trace = []
+        eng.link.set_trace(True)
+        self.ref = None
+
+    def begin(self) -> None:
+        torch.cuda.synchronize(self.eng.device)
+        self.ref = torch.cuda.Event(enable_timing=True)
+        self.ref.record()
+        self.eng.cache.trace.clear()
+        self.eng.link.trace_read(self.ref)                # drop spans of earlier steps
+        self.k0 = {n: len(v) for n, v in self.eng.prof.spans.items()}
+
+    def end(self) -> dict:
+        end = torch.cuda.Event(enable_timing=True)
+        end.record()
+        torch.cuda.synchronize(self.eng.device)
+        ref = self.ref
+        copies = [(ref.elapsed_time(a), ref.elapsed_time(b)) for a, b in self.eng.cache.trace]
+        copies += self.eng.link.trace_read(ref)
+        comp = []
+        for n, v in self.eng.prof.spans.items():
+            comp += [(ref.elapsed_time(a), ref.elapsed_time(b)) for a, b, _, _ in v[self.k0.get(n, 0):]]
+        u = _union(copies)
+        busy = sum(b - a for a, b in u)
+        total = ref.elapsed_time(end)
+        ct = sum(b - a for a, b in comp)
+        hidden = sum(_covered(a, b, u) for a, b in comp)
+        return {"step_ms": total, "copy_busy_ms": busy, "copy_busy_frac": busy / total if total else None,
+                "expert_compute_ms": ct, "overlap_frac": hidden / ct if ct else None,
+                "n_copy_spans": len(copies), "n_compute_spans": len(comp)}
 
 
 class KernelProfiler:

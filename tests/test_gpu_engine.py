@@ -119,6 +119,21 @@ def test_ondemand_policy_same_tokens(tiny, cuda):
     assert eng.n_slots == 2
 
 
+def test_prefetchall_policy_same_tokens_and_log(tiny, cuda):
+    """MoESys baseline: all M experts of every layer visit streamed into two banks of M slots."""
+    shape = tiny["shape"]
+    L = shape.num_layers
+    eng = Engine(shape, "prefetchall", seed=3, dense=tiny["dense"].to(cuda), max_seq=PREFILL + DECODE + 8,
+                 max_prefill=PREFILL)
+    assert eng.n_slots == 16
+    assert eng.generate(tiny["ids"], DECODE) == tiny["toks"]
+    pre = [tuple(tuple(int(e) for e in eng.paths_prefill[t, l]) for l in range(L)) for t in range(PREFILL)]
+    exp = sim_ref.cache_log_prefill(pre, L, "prefetchall", M=8) + \
+        sim_ref.cache_log_decode(eng.paths_decode, None, L, "prefetchall", M=8)[0]
+    assert eng.log == exp
+    assert eng.paths_decode == tiny["eng"].paths_decode
+
+
 def test_faithful_and_cancelling_schedules_agree(tiny, cuda):
     """Chunked cancellable prefetch changes transfers, not decisions: same tokens, same cache log."""
     shape = tiny["shape"]

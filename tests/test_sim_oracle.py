@@ -35,6 +35,11 @@ def test_cache_log_semantics():
     assert log[1]["refetch"] == [] and log[2]["refetch"] == [5]
     assert log[4]["refetch"] == [3, 4]
     assert cnt["prefetch_hits"] + cnt["prefetch_misses"] == 2 * 2 * 2
+    pa, cnt = sim_ref.cache_log_decode(paths, None, 3, "prefetchall", M=8)
+    assert all(r["fetch"] == list(range(8)) and r["kind"] == "prefetchall" for r in pa) and len(pa) == 6
+    assert cnt["prefetch_hits"] == cnt["prefetch_misses"] == 0
+    pa = sim_ref.cache_log_prefill([((0, 1), (2, 3))], 2, "prefetchall", owned=[1, 3, 5, 7])
+    assert pa[1]["fetch"] == [1, 3, 5, 7] and pa[1]["activated"] == [2, 3]
     pre = sim_ref.cache_log_prefill([((0, 1), (2, 3)), ((1, 2), (3, 5))], 2)
     assert pre[0]["fetch"] == [0, 1, 2] and pre[1]["fetch"] == [0, 2, 3, 5] and pre[1]["activated"] == [2, 3, 5]
 
