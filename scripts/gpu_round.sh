@@ -16,6 +16,10 @@ for s in $STEPS; do
     bench)  log bench;  timeout 1500 python bench.py --steps 2 --warmup 3 --out gpurun_out/bench.json > gpurun_out/bench.log 2>&1; log "bench rc=$?";;
     bench22) log bench22; timeout 2400 python bench.py --config mixtral-8x22b --steps 1 --warmup 3 --warmup-decode 8 --no-cpu-baseline --out gpurun_out/bench22.json > gpurun_out/bench22.log 2>&1; log "bench22 rc=$?";;
     benchref) log benchref; timeout 600 python bench.py --impl reference --steps 1 --warmup 1 > gpurun_out/bench_ref.log 2>&1; log "benchref rc=$?";;
+    sweep)  log sweep;  timeout 900 python scripts/sweep.py --out gpurun_out/sweep.json > gpurun_out/sweep.log 2>&1; log "sweep rc=$?";;
+    benchpa) log benchpa; timeout 1500 python bench.py --policy prefetchall --steps 1 --warmup 3 --decode 32 --warmup-decode 4 --no-cpu-baseline --out gpurun_out/bench_pa.json > gpurun_out/bench_pa.log 2>&1; log "benchpa rc=$?";;
+    benchod) log benchod; timeout 1500 python bench.py --policy ondemand --steps 1 --warmup 3 --decode 32 --warmup-decode 4 --no-cpu-baseline --out gpurun_out/bench_od.json > gpurun_out/bench_od.log 2>&1; log "benchod rc=$?";;
+    benchor) log benchor; timeout 1500 python bench.py --policy oracle --steps 1 --warmup 3 --decode 32 --warmup-decode 4 --no-cpu-baseline --out gpurun_out/bench_or.json > gpurun_out/bench_or.log 2>&1; log "benchor rc=$?";;
     kbench) log kbench; timeout 600 python scripts/kbench.py --iters 20 > gpurun_out/kbench.json 2> gpurun_out/kbench.err; log "kbench rc=$?";;
     launches)
       log launches
