@@ -47,6 +47,7 @@ from .model import (DenseWeights, KVCache, attention_block, attention_decode_sta
                     logits_last, rms_norm, rope_tables)
 from .ep import EPConfig, owned_experts, owner_mask
 from .predictor import ExpertMLP, StatsOnDevice, _mode_code
+from .stats import OnlineRoutingStats
 
 
 class HostExpertStore:
@@ -314,7 +315,7 @@ class Engine:
                  predictor: ExpertMLP | None = None, pop=None, aff=None, oracle_paths=None,
                  max_seq: int = 2048, max_prefill: int = 2048, cancel_mispredicted: bool = True,
                  chunk_mb: float = 4.0, link_depth: int = 2, use_graphs: bool = True,
-                 ep: EPConfig | None = None):
+                 ep: EPConfig | None = None, collect_stats: bool = False):
         self.shape = shape
         self.policy = SchedulerPolicy(policy)
         self.device = torch.device(device)
@@ -370,6 +371,9 @@ class Engine:
         ws = max(ops.grouped_ffn_workspace(r, self.d, self.ff) for r in (P * self.k // 4, P * self.k))
         self.p_ws = torch.empty(max(ws, 256), dtype=torch.uint8, device=dev)
         self.prefill_idx_host = None
+        # online routing statistics: device counters fed by the gate
+        self.route_stats = OnlineRoutingStats(self.L, self.M, self.k, dev) if collect_stats else None
+        self.p_paths = torch.empty((P, self.L, self.k), dtype=torch.int32, device=dev) if collect_stats else None
         self.capture = None          # debug/parity: list of (phase, layer, gate input, idx)
         self.use_graphs = use_graphs
         self.g_graphs = None
@@ -422,6 +426,8 @@ class Engine:
             idx_all.append(idx_host)
         self.kv.len = T
         self.paths_prefill = np.stack(idx_all, axis=1)     # [T, L, k]
+        if self.route_stats is not None:
+            self.route_stats.add(self.p_paths[:T])
         lg = logits_last(self.shape, self.W, h[-1:])[0]
         self.last_logits = lg
         tok = int(torch.argmax(lg).item())
@@ -456,6 +462,8 @@ class Engine:
             path.append(tuple(E))
         self.kv.len = pos + 1
         self.paths_decode.append(tuple(path))
+        if self.route_stats is not None:                   # hist holds idx + 1 of every layer
+            self.route_stats.add((self.hist.view(1, self.L, self.k) - 1).to(torch.int32))
         lg = logits_last(self.shape, self.W, h)[0]
         self.last_logits = lg
         tok = int(torch.argmax(lg).item())
@@ -552,6 +560,8 @@ class Engine:
         a = rms_norm(h, self.W.layers[l]["ln2"], sh.rms_eps)
         idx, w = self.p_idx[:T], self.p_w[:T]
         ops.gate_topk(a, self.W.layers[l]["wg"], self.k, idx, w)
+        if self.p_paths is not None:
+            self.p_paths[:T, l].copy_(idx)
         if self.capture is not None:
             self.capture.append(("prefill", l, a.cpu(), idx.cpu()))
         ops.permute(idx, a, self.M, self.p_off, self.p_pos[:T * self.k], self.p_src[:T * self.k],

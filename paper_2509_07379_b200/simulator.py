@@ -241,7 +241,8 @@ def gpu_only_memory(cfg: ModelConfig) -> int:
 class _State:
     """Mutable per-request simulation state: stream clocks, cache, log."""
 
-    def __init__(self, policy: SchedulerPolicy, cfg: ModelConfig, cost: CostModel):
+    def __init__(self, policy: SchedulerPolicy, cfg: ModelConfig, cost: CostModel,
+                 prefill_non_moe_s: float | None = None):
         self.policy, self.cfg, self.cost = policy, cfg, cost
         self.tl = EventTimeline()
         self.cache = DeviceExpertCache(slot_count(policy, cfg))
@@ -250,6 +251,9 @@ class _State:
         self.t_predict = 0
         self.T = _ns(cost.transfer_time_s(cfg.expert_bytes))
         self.nm = _ns(cost.non_moe_compute_per_layer_s)
+        # B200 extension: the reference CostModel has one non-MoE time per layer;
+        # a calibrated model may give the (T-token) prefill pass its own
+        self.nm_prefill = self.nm if prefill_non_moe_s is None else _ns(prefill_non_moe_s)
         self.gate = _ns(cost.gate_compute_s)
         self.pred = _ns(cost.predictor_latency_s)
         self.log: list = []
@@ -287,9 +291,10 @@ class _State:
 
     def non_moe_and_gate(self, **payload) -> tuple[int, int]:
         t0 = self.t_compute
-        self.tl.add("compute", "non_moe", t0, t0 + self.nm, **payload)
-        self.tl.add("compute", "gate", t0 + self.nm, t0 + self.nm + self.gate, **payload)
-        self.t_compute = t0 + self.nm + self.gate
+        nm = self.nm_prefill if payload.get("phase") == "prefill" else self.nm
+        self.tl.add("compute", "non_moe", t0, t0 + nm, **payload)
+        self.tl.add("compute", "gate", t0 + nm, t0 + nm + self.gate, **payload)
+        self.t_compute = t0 + nm + self.gate
         return t0, self.t_compute
 
 
@@ -405,12 +410,14 @@ def _requests(traces) -> list:
 
 
 def simulate_request(policy, traces, cfg: ModelConfig, cost: CostModel, net=None, pop=None, aff=None,
-                     seed: int = 0, check: bool = True):
+                     seed: int = 0, check: bool = True, prefill_non_moe_s: float | None = None):
     """Simulate one request (its prefill + decode traces) under a policy.
 
     net: a predictor object with ``predict(trace, l) -> tuple`` (the
     reference protocol, predictor.py:424-510); required by ``duoserve``;
     ``oracle`` predicts the true selection with zero prediction latency.
+    prefill_non_moe_s: optional non-MoE time of a prefill layer (B200
+    calibration; default: cost.non_moe_compute_per_layer_s as in the SPEC).
     Returns (RequestMetrics, EventTimeline, cache log)."""
     pol = SchedulerPolicy(policy)
     traces = list(traces)
@@ -430,7 +437,7 @@ def simulate_request(policy, traces, cfg: ModelConfig, cost: CostModel, net=None
             raise ConfigError("policy duoserve needs a predictor")
         if hasattr(net, "input_dim") and not hasattr(net, "predict"):
             raise ConfigError("pass a predictor object (MLPPredictor / PrecomputedPredictor), not a raw network")
-    st = _State(pol, cfg, cost)
+    st = _State(pol, cfg, cost, prefill_non_moe_s)
     for l in range(L):
         act: dict = {}
         for tr in pre:

@@ -132,3 +132,55 @@ def export_csv(pop: PopularityMatrix, aff: AffinityMatrix, out_dir) -> list[Path
         write(out_dir / f"affinity_l{l}_l{l + 1}.csv", ["expert"] + [f"next_{j}" for j in range(M)],
               [[i] + [repr(float(v)) for v in aff.values[l, i]] for i in range(M)])
     return files
+
+
+# --------------------------------------------------------------------------
+# Online collection on the device ("data
+# collection and inference serving ... simultaneously")
+
+class OnlineRoutingStats:
+    """int64 popularity / affinity counters in HBM, fed with gate selections
+    [N, L, k] by the ``ds_route_histogram`` kernel while serving.  Integer
+    counting is order independent, so ``matrices()`` equals
+    ``build_popularity`` / ``build_affinity`` over the same selections bit for
+    bit (stats.py:52-71)."""
+
+    def __init__(self, L: int, M: int, k: int, device):
+        import torch
+        if L < 2:
+            raise StatsError(f"affinity needs at least 2 layers, model has {L}")
+        self.L, self.M, self.k = L, M, k
+        self.pop_counts = torch.zeros((L, M), dtype=torch.int64, device=device)
+        self.aff_counts = torch.zeros((L - 1, M, M), dtype=torch.int64, device=device)
+        self.n_episodes = 0
+
+    def add(self, paths) -> None:
+        """paths: device int32 [N, L, k] of expert indices."""
+        from . import ops
+        if paths.dim() != 3 or tuple(paths.shape[1:]) != (self.L, self.k):
+            raise StatsError(f"paths must be [N, {self.L}, {self.k}], got {tuple(paths.shape)}")
+        if paths.shape[0] == 0:
+            return
+        ops.route_histogram(paths.contiguous(), self.M, self.pop_counts, self.aff_counts)
+        self.n_episodes += int(paths.shape[0])
+
+    def reset(self) -> None:
+        self.pop_counts.zero_()
+        self.aff_counts.zero_()
+        self.n_episodes = 0
+
+    def matrices(self) -> tuple[PopularityMatrix, AffinityMatrix]:
+        if self.n_episodes == 0:
+            raise StatsError("no routing collected yet")
+        return (normalize_popularity(self.pop_counts.cpu().numpy(), self.n_episodes),
+                normalize_affinity(self.aff_counts.cpu().numpy()))
+
+
+def count_on_device(ds: TraceDataset, device="cuda") -> tuple[PopularityMatrix, AffinityMatrix]:
+    """build_popularity + build_affinity with the counting on the GPU."""
+    import torch
+    if not ds.traces:
+        raise StatsError("cannot build popularity from an empty dataset")
+    st = OnlineRoutingStats(ds.L, ds.M, ds.k, device)
+    st.add(torch.as_tensor(ds.paths_array().astype(np.int32), device=device))
+    return st.matrices()

@@ -142,3 +142,29 @@ def test_faithful_and_cancelling_schedules_agree(tiny, cuda):
     assert eng.generate(tiny["ids"], DECODE) == tiny["toks"]
     assert eng.log == tiny["eng"].log
     assert tiny["eng"].cancel_mispredicted and not eng.cancel_mispredicted
+
+
+def test_online_routing_stats_equal_reference_counting(tiny, cuda):
+    """pop/aff counted on the device from the served
+    routing equal build_popularity / build_affinity (stats.py:52-71) over the
+    same selections, bit for bit; count_on_device equals them on a dataset."""
+    shape = tiny["shape"]
+    L = shape.num_layers
+    eng = Engine(shape, "duoserve", seed=3, dense=tiny["dense"].to(cuda), predictor=tiny["net"], pop=tiny["pop"],
+                 aff=tiny["aff"], max_seq=PREFILL + DECODE + 8, max_prefill=PREFILL, collect_stats=True)
+    assert eng.generate(tiny["ids"], DECODE) == tiny["toks"]
+    pre = [T.ActivationTrace(0, "prefill", t, tuple(tuple(sorted(int(e) for e in eng.paths_prefill[t, l]))
+                                                   for l in range(L))) for t in range(PREFILL)]
+    dec = [T.ActivationTrace(0, "decode", PREFILL + t, tuple(tuple(sorted(p)) for p in path))
+           for t, path in enumerate(eng.paths_decode)]
+    ds = T.TraceDataset(shape.name, L, 8, 2, pre + dec)
+    pop, aff = eng.route_stats.matrices()
+    rp, ra = S.build_popularity(ds), S.build_affinity(ds)
+    assert np.array_equal(pop.counts, rp.counts) and np.array_equal(pop.values, rp.values)
+    assert np.array_equal(aff.counts, ra.counts) and np.array_equal(aff.values, ra.values)
+    assert pop.n_episodes == rp.n_episodes == PREFILL + len(eng.paths_decode)
+    cfg, _ = C.load_preset("tiny-4x8")
+    big = T.generate_traces(T.default_generator_params(4, 8, 0.8, seed=21), cfg, 32, 32, 32)
+    dp, da = S.count_on_device(big, cuda)
+    assert np.array_equal(dp.counts, S.build_popularity(big).counts)
+    assert np.array_equal(da.values, S.build_affinity(big).values)
