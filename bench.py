@@ -128,6 +128,14 @@ def measured_peaks() -> dict:
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "_fallback": True}
 
 
+def ncu_traffic() -> dict:
+    """DRAM bytes (read + write) per roofline unit from the committed ncu
+    --set full captures (profiles/ncu_traffic.json, written by
+    scripts/ncu_traffic.py), keyed like KernelProfiler's kernel names."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    return json.loads(p.read_text()) if p.exists() else {}
+
+
 def predictor_inputs(shape, seed: int = 0):
     """ExpertMLP(d_in, 8, seed=0) + pop/aff from generate_traces(default_generator_params(L, 8, 0.8, seed=7))
     (SURVEY.md §8d)."""
@@ -340,6 +348,13 @@ def run_ours(args):
     h2d_step = r0["h2d_experts"] + args.prefill * 8
     prof.spans = {n: v[:n_spans[n]] for n, v in prof.spans.items() if n in n_spans}
     kern = prof.summary(peaks)
+    traffic = ncu_traffic()
+    for kk in kern["all"] + ([kern["dominant"]] if kern["dominant"] else []):
+        kk["peak_of"] = "fallback (B200_PROFILING.md)" if peaks.get("_fallback") else "measured (MEASURED_PEAKS.json)"
+        t = traffic.get(kk["kernel"])
+        if t is not None:
+            kk["traffic"] = t["bytes_per_unit"]
+            kk["traffic_source"] = t["source"]
     res_b = eng.resident_bytes()
     peak_dev = torch.cuda.max_memory_allocated(dev)
     line = {

@@ -20,17 +20,18 @@ for s in $STEPS; do
     benchpa) log benchpa; timeout 1500 python bench.py --policy prefetchall --steps 1 --warmup 3 --decode 32 --warmup-decode 4 --no-cpu-baseline --out gpurun_out/bench_pa.json > gpurun_out/bench_pa.log 2>&1; log "benchpa rc=$?";;
     benchod) log benchod; timeout 1500 python bench.py --policy ondemand --steps 1 --warmup 3 --decode 32 --warmup-decode 4 --no-cpu-baseline --out gpurun_out/bench_od.json > gpurun_out/bench_od.log 2>&1; log "benchod rc=$?";;
     benchor) log benchor; timeout 1500 python bench.py --policy oracle --steps 1 --warmup 3 --decode 32 --warmup-decode 4 --no-cpu-baseline --out gpurun_out/bench_or.json > gpurun_out/bench_or.log 2>&1; log "benchor rc=$?";;
+    calib)  log calib;  timeout 900 python scripts/calibrate_cost.py --out gpurun_out/calib.json > gpurun_out/calib.log 2>&1; log "calib rc=$?";;
     kbench) log kbench; timeout 600 python scripts/kbench.py --iters 20 > gpurun_out/kbench.json 2> gpurun_out/kbench.err; log "kbench rc=$?";;
     launches)
       log launches
       timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "timed/" \
         --csv --log-file gpurun_out/launches.csv \
-        python bench.py --steps 1 --warmup 1 --decode 16 --warmup-decode 2 --no-cpu-baseline > gpurun_out/launches.log 2>&1
+        python bench.py --steps 1 --warmup 1 --decode 4 --warmup-decode 2 --no-cpu-baseline > gpurun_out/launches.log 2>&1
       log "launches rc=$?"
       python scripts/summarize_launches.py gpurun_out/launches.csv > gpurun_out/launches_summary.md 2>&1;;
     ncu)
       log ncu
-      timeout 900 ncu --set full --clock-control none --import-source on -k regex:'swiglu_gemv|down_gemv' -s 8 -c 2 \
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:'mma_gemv|swiglu_gemv|down_gemv' -s 8 -c 2 \
         -o gpurun_out/k4 -f python scripts/kbench.py --only k4 --iters 3 > gpurun_out/ncu_k4.log 2>&1
       log "ncu k4 rc=$?"
       timeout 900 ncu --set full --clock-control none --import-source on -k regex:'w4_gemm' -s 4 -c 2 \

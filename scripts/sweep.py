@@ -81,18 +81,19 @@ rw = torch.ones(maxR, device=dev)
 y = torch.empty(maxR, d, device=dev)
 ws = torch.empty(max(ops.grouped_ffn_workspace(maxR, d, ff), 256), dtype=torch.uint8, device=dev)
 for R in rows_list:
+    # K4 takes <= 64 activation rows per call (decode batches); beyond that only K3
     t4 = timeit(lambda i: (ops.swiglu_gemv(x[:R], es[i % NB], d, ff, G, hbuf[:R]),
-                           ops.down_gemv(hbuf[:R], es[i % NB], d, ff, G, rw, 1, acc[:R])))
+                           ops.down_gemv(hbuf[:R], es[i % NB], d, ff, G, rw, 1, acc[:R]))) if R <= 64 else float("inf")
     t3 = timeit(lambda i: ops.grouped_ffn(x[:R], [0, R], [es[i % NB]], d, ff, G, hbuf[:R], y[:R], ws))
     fl = 6.0 * R * d * ff
-    per_rows[R] = {"k4_us": round(t4 * 1e6, 2), "k3_us": round(t3 * 1e6, 2),
+    per_rows[R] = {"k4_us": round(t4 * 1e6, 2) if t4 < float("inf") else None, "k3_us": round(t3 * 1e6, 2),
                    "k4_GBs": round(total / t4 / 1e9, 1), "k3_TFLOPs": round(fl / t3 / 1e12, 1),
                    "best": "K4 gemv" if t4 < t3 else "K3 tcgen05"}
     print(R, per_rows[R], flush=True)
 
 
 def interp(R: float, key: str) -> float:
-    rs = sorted(per_rows)
+    rs = sorted(r for r in per_rows if per_rows[r][key] is not None)
     if R <= rs[0]:
         return per_rows[rs[0]][key] * 1e-6
     for lo, hi in zip(rs, rs[1:]):
@@ -122,7 +123,8 @@ for B in (1, 2, 4, 8, 16, 32):
                        "decode_kernel": "K3" if interp(rows_d, "k3_us") < interp(rows_d, "k4_us") else "K4",
                        "decode_moe_compute_ms_per_layer": round(1e3 * comp_d, 3),
                        "decode_link_ms_per_layer": round(1e3 * Ad * link_t, 3)})
-crossover = next((R for R in rows_list if per_rows[R]["k3_us"] < per_rows[R]["k4_us"]), None)
+crossover = next((R for R in rows_list if per_rows[R]["k4_us"] is None or per_rows[R]["k3_us"] < per_rows[R]["k4_us"]),
+                 None)
 out = {"shape": sh.name, "expert_bytes": total, "h2d_GBs": round(h2d, 2), "per_rows": per_rows,
        "k3_beats_k4_from_rows": crossover, "points": points}
 Path(a.out).parent.mkdir(parents=True, exist_ok=True)
