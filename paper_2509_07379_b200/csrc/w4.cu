@@ -20,6 +20,8 @@
 // warp-shuffle reduction, SwiGLU / routing-weight epilogue fused.
 #include "ds_common.cuh"
 
+#include <cstdlib>
+
 namespace ds {
 namespace {
 
@@ -208,6 +210,7 @@ __global__ void __launch_bounds__(kGemvThreads, 2) swiglu_gemv_kernel(
     extern __shared__ __align__(16) uint32_t sm[];
     uint32_t* xs = sm;
     float* xsum = reinterpret_cast<float*>(sm + R * K / 2);
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // the down GEMV may launch early
     stage_x(x, R, K, xs, xsum);
     const int lane = threadIdx.x & 31;
     const int warps = gridDim.x * (blockDim.x >> 5);
@@ -233,6 +236,7 @@ __global__ void __launch_bounds__(kGemvThreads, 2) down_gemv_kernel(
     extern __shared__ __align__(16) uint32_t sm[];
     uint32_t* xs = sm;
     float* xsum = reinterpret_cast<float*>(sm + R * K / 2);
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // h comes from the SwiGLU GEMV (PDL launch)
     stage_x(hin, R, K, xs, xsum);
     const int lane = threadIdx.x & 31;
     const int warps = gridDim.x * (blockDim.x >> 5);
@@ -248,6 +252,261 @@ __global__ void __launch_bounds__(kGemvThreads, 2) down_gemv_kernel(
             }
         }
     }
+}
+
+// ------------------------------------------------- GEMV v3 (K4, mma.sync)
+// G = 128.  The int4 -> bf16 dequant stays on the CUDA cores (7 ALU ops per
+// 8 codes: the (128 + q) exponent trick) but the multiply-accumulate moves to
+// the tensor cores: one mma.m16n8k16 consumes 16 weight rows x 16 k with the
+// activation rows (<= 8 tokens) on the N side.  A CTA owns one 16-row block
+// of the output; its S warps split K into runs of whole groups, so every
+// warp-step is exactly one quantisation group (4 lanes x 32 codes per row):
+//   lane (g, t) = (lane / 4, lane % 4) loads the 16-byte code chunk t of
+//   rows g and g + 8 of the group; its 32 codes are the A fragments of 8 mmas
+//   and the same k positions of x (64 contiguous bytes) its B fragments:
+//   mma j = (word w, half s): a = {P_g[w][2s], P_g+8[w][2s], P_g[w][2s+1],
+//   P_g+8[w][2s+1]} with P_r[w][i] = (128 + q) pair i of word w of row r,
+//   b = x[c0 + 32t + 8w + 4s .. +4).  The k permutation inside an mma is the
+//   same for A and B, so the dot product is unchanged.
+// A ninth fragment set with A = 1.0 gives sum_k x per token and group, so
+//   sum_k x (q - z) s = s * ( D - (128 + z) * sum_k x )
+// (the same factorisation as v2, exact products (q - z) s).  Loads run P
+// groups ahead in a register ring; the S per-warp partials are reduced in
+// shared memory in a fixed order (deterministic).
+constexpr int kTok = 8;  // activation rows per pass (mma N)
+
+__device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// Per-lane stream pointers, positioned at the warp's first group.
+template <int NMAT>
+struct GroupPtrs {
+    const uint4* c[NMAT][2];
+    const uint4* x;
+};
+
+__device__ __forceinline__ void cp_async16(uint32_t smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// codes of group j -> this lane's ring slot (lane-private: no warp sync needed)
+template <int NMAT>
+__device__ __forceinline__ void issue_codes(uint32_t slot, const GroupPtrs<NMAT>& q, int j) {
+#pragma unroll
+    for (int m = 0; m < NMAT; ++m)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) cp_async16(slot + (uint32_t)(m * 2 + h) * 512u, q.c[m][h] + 4 * j);
+}
+
+// x[tok][c0 + 32 t .. + 32) of group j: re-read by every row block, so it
+// comes from L1 / L2; loaded one group ahead of its use
+__device__ __forceinline__ void load_x(uint4 (&xv)[4], const uint4* __restrict__ x, int j) {
+#pragma unroll
+    for (int w = 0; w < 4; ++w) xv[w] = __ldg(x + 16 * j + w);
+}
+
+template <int NMAT>
+__device__ __forceinline__ void mma_group(const uint4 (&c)[NMAT][2], const uint4 (&xv)[4],
+                                          const uint16_t* __restrict__ sm_s, const uint8_t* __restrict__ sm_z,
+                                          int ngw, int g, int j, float (&acc)[NMAT][4]) {
+    // CH independent accumulator chains per matrix (and for sum x) cut the
+    // dependent-HMMA latency per group; with NMAT = 2 the W1 / W3 chains
+    // already interleave
+    constexpr int CH = NMAT == 1 ? 2 : 1;
+    float dx[CH][4] = {};
+    float d[NMAT][CH][4] = {};
+    constexpr uint32_t kOne = 0x3F803F80u;  // bf16 {1.0, 1.0}
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+        const uint32_t xw[4] = {xv[w].x, xv[w].y, xv[w].z, xv[w].w};
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            mma16816(dx[s % CH], kOne, kOne, kOne, kOne, xw[2 * s], xw[2 * s + 1]);
+#pragma unroll
+            for (int m = 0; m < NMAT; ++m) {
+                const uint32_t* cg = reinterpret_cast<const uint32_t*>(&c[m][0]);
+                const uint32_t* cg8 = reinterpret_cast<const uint32_t*>(&c[m][1]);
+                mma16816(d[m][s % CH], nib_pair_magic(cg[w] >> (8 * s)), nib_pair_magic(cg8[w] >> (8 * s)),
+                         nib_pair_magic(cg[w] >> (8 * s + 4)), nib_pair_magic(cg8[w] >> (8 * s + 4)),
+                         xw[2 * s], xw[2 * s + 1]);
+            }
+        }
+    }
+    float xs0 = dx[0][0], xs1 = dx[0][1];
+#pragma unroll
+    for (int c2 = 1; c2 < CH; ++c2) xs0 += dx[c2][0], xs1 += dx[c2][1];
+    // rows g (regs 0, 1) and g + 8 (regs 2, 3); tokens 2t (even regs), 2t + 1 (odd)
+#pragma unroll
+    for (int m = 0; m < NMAT; ++m) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            // per-warp staged scale (bf16 bits) and zero (0..15) of row g + 8h, group j
+            const int si = (m * 16 + g + 8 * h) * ngw + j;
+            const float z128 = __uint_as_float(0x43000000u | ((uint32_t)sm_z[si] << 16));   // 128 + z
+            const float sc = __uint_as_float((uint32_t)sm_s[si] << 16);
+            float v0 = d[m][0][2 * h], v1 = d[m][0][2 * h + 1];
+#pragma unroll
+            for (int c2 = 1; c2 < CH; ++c2) v0 += d[m][c2][2 * h], v1 += d[m][c2][2 * h + 1];
+            acc[m][2 * h] = fmaf(sc, fmaf(-z128, xs0, v0), acc[m][2 * h]);
+            acc[m][2 * h + 1] = fmaf(sc, fmaf(-z128, xs1, v1), acc[m][2 * h + 1]);
+        }
+    }
+}
+
+// ring bytes per warp: P stages x NMAT matrices x 2 row halves x 32 lanes x 16 B
+template <int NMAT, int P>
+constexpr int mma_gemv_ring_bytes() { return P * NMAT * 2 * 512; }
+// staged scales (2 B) + zeros (1 B) per warp: NMAT x 16 rows x ngw groups
+__host__ __device__ inline int mma_gemv_aux_bytes(int nmat, int ngw) { return (nmat * 16 * ngw * 3 + 15) & ~15; }
+
+// One CTA per 16-row block; warp s streams groups [s*ngw, min((s+1)*ngw, NG)).
+// NMAT = 2: h[r, n] = bf16(silu(x_r . W1[:, n]) * (x_r . W3[:, n]));
+// NMAT = 1: out[r, n] += route_w[r] * (x_r . W2[:, n]).
+// The code stream (the HBM bytes) runs P groups ahead through a lane-private
+// cp.async ring in shared memory, so the depth costs no registers; scales /
+// zeros and x run one group ahead in registers.
+template <int NMAT, int P>
+__global__ void __launch_bounds__(NMAT == 2 ? 64 : 256, NMAT == 2 ? 7 : 1) mma_gemv_kernel(const __nv_bfloat16* __restrict__ x, int R, W4Ptr wa,
+                                                       W4Ptr wb, int K, int N, int ngw,
+                                                       __nv_bfloat16* __restrict__ h,
+                                                       const float* __restrict__ route_w, int route_stride,
+                                                       float* __restrict__ out) {
+    static_assert(P % 2 == 0, "aux / x are double-buffered by the parity of the unrolled stage index");
+    extern __shared__ __align__(16) uint8_t gemv_smem[];
+    __shared__ float red[NMAT == 2 ? 2 : 8][NMAT][4][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, S = blockDim.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int NG = K >> 7;
+    const int rowg = blockIdx.x * 16 + g;
+    const int gbeg = warp * ngw;
+    const int nsteps = max(0, min(ngw, NG - gbeg));
+    // B columns of tokens >= R read row R - 1 (same addresses: a broadcast);
+    // their D columns are never stored
+    const int tok = g < R ? g : R - 1;
+    GroupPtrs<NMAT> q;
+#pragma unroll
+    for (int m = 0; m < NMAT; ++m) {
+        const W4Ptr W = (m == 0) ? wa : wb;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+            const int row = rowg + 8 * hh;
+            q.c[m][hh] = reinterpret_cast<const uint4*>(W.codes + (size_t)row * (K >> 3)) + gbeg * 4 + t;
+        }
+    }
+    q.x = reinterpret_cast<const uint4*>(x + (size_t)tok * K) + gbeg * 16 + 4 * t;
+    // lane-private ring: slot (stage p, matrix m, half h) at p*NMAT*1024 + (2m+h)*512 + lane*16
+    const uint32_t ring = (uint32_t)__cvta_generic_to_shared(gemv_smem) +
+                          (uint32_t)warp * mma_gemv_ring_bytes<NMAT, P>() + lane * 16u;
+    const uint8_t* ring_ptr = gemv_smem + warp * mma_gemv_ring_bytes<NMAT, P>() + lane * 16;
+    // the warp's scales (bf16) and zeros (0..15) for its 16 rows x ngw groups,
+    // staged once behind the rings (no per-group scattered 2-byte loads)
+    const int aux_bytes = mma_gemv_aux_bytes(NMAT, ngw);
+    uint16_t* sm_s = reinterpret_cast<uint16_t*>(gemv_smem + S * mma_gemv_ring_bytes<NMAT, P>() + warp * aux_bytes);
+    uint8_t* sm_z = reinterpret_cast<uint8_t*>(sm_s + NMAT * 16 * ngw);
+    // programmatic dependent launch: let the next kernel (the down projection
+    // after the SwiGLU GEMV) be scheduled as SMs free up; everything before
+    // griddepcontrol.wait touches only weights, never the previous kernel's output
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    for (int i = lane; i < NMAT * 16 * nsteps; i += 32) {
+        const int m = i / (16 * nsteps), rem = i - m * 16 * nsteps, r = rem / nsteps, jj = rem - r * nsteps;
+        const W4Ptr W = (m == 0) ? wa : wb;
+        const int zi = (blockIdx.x * 16 + r) * NG + gbeg + jj;
+        sm_s[(m * 16 + r) * ngw + jj] = __ldg(W.scales + zi);
+        sm_z[(m * 16 + r) * ngw + jj] = (__ldg(W.zeros + (zi >> 1)) >> ((zi & 1) << 2)) & 15;
+    }
+    __syncwarp();
+
+    float acc[NMAT][4];
+#pragma unroll
+    for (int m = 0; m < NMAT; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0.f;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        if (p < nsteps) issue_codes<NMAT>(ring + (uint32_t)p * NMAT * 1024u, q, p);
+        cp_async_commit();                  // (possibly empty) group p
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // x (and out) come from the previous kernel
+    uint4 xv[2][4];
+    if (nsteps > 0) load_x(xv[0], q.x, 0);
+    for (int s0 = 0; s0 < nsteps; s0 += P) {
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const int j = s0 + p;
+            if (j < nsteps) {
+                if (j + 1 < nsteps) load_x(xv[(p + 1) & 1], q.x, j + 1);
+                cp_async_wait<P - 1>();      // this lane's group j landed
+                uint4 c[NMAT][2];
+#pragma unroll
+                for (int m = 0; m < NMAT; ++m)
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh)
+                        c[m][hh] = *reinterpret_cast<const uint4*>(ring_ptr + p * NMAT * 1024 + (m * 2 + hh) * 512);
+                if (j + P < nsteps) issue_codes<NMAT>(ring + (uint32_t)p * NMAT * 1024u, q, j + P);
+                cp_async_commit();
+                mma_group<NMAT>(c, xv[p & 1], sm_s, sm_z, ngw, g, j, acc);
+            }
+        }
+    }
+    if (S > 1) {
+#pragma unroll
+        for (int m = 0; m < NMAT; ++m)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) red[warp][m][i][lane] = acc[m][i];
+        __syncthreads();
+        if (warp != 0) return;
+#pragma unroll
+        for (int m = 0; m < NMAT; ++m)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                float v = red[0][m][i][lane];
+                for (int w = 1; w < S; ++w) v += red[w][m][i][lane];
+                acc[m][i] = v;
+            }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int row = rowg + 8 * (i >> 1);
+        const int tk = 2 * t + (i & 1);
+        if (tk < R) {
+            if constexpr (NMAT == 2) {
+                const float av = acc[0][i], bv = acc[1][i];
+                h[(size_t)tk * N + row] = __float2bfloat16_rn(av / (1.0f + expf(-av)) * bv);
+            } else {
+                float* o = out + (size_t)tk * N + row;
+                *o = __fadd_rn(*o, __fmul_rn(route_w[(size_t)tk * route_stride], acc[0][i]));
+            }
+        }
+    }
+}
+
+// Warps per CTA.  SwiGLU (NMAT = 2, N/16 = 896..1024 row blocks): 2 warps,
+// so that all ~7 CTAs per SM are resident at once (one wave: no tail wave of
+// a few row blocks).  Down (256..384 row blocks): up to 8 warps splitting K.
+// Variant choice for G = 128 (measured on B200, scripts/kbench.py, one
+// expert of 8x7B): at R = 1 the warp-per-row FHFMA GEMV (v2) streams the
+// expert in 39.8 us against 43.9 us for the mma.sync GEMV, which is
+// latency-bound at one token; the mma.sync GEMV carries up to 8 activation
+// rows per pass at the cost of one (tokens sit on the mma N side), so it
+// takes every R >= 2.  DS_K4_VARIANT=v2|mma forces one (A/B benchmarks).
+inline bool k4_use_mma(int R) {
+    static const char* v = getenv("DS_K4_VARIANT");
+    if (v && v[0] == 'v') return false;
+    if (v && v[0] == 'm') return true;
+    return R >= 2;
+}
+
+inline int mma_gemv_warps(int NG, int nmat) {
+    if (nmat == 2) return NG >= 2 ? 2 : 1;
+    int S = (NG + 7) / 8;
+    return S < 1 ? 1 : (S > 8 ? 8 : S);
 }
 
 __global__ void finalize_kernel(float* __restrict__ acc, const __nv_bfloat16* __restrict__ resid,
@@ -360,7 +619,17 @@ static int down_launch_u(const __nv_bfloat16* h, const ds_w4_expert* e, int d, i
     }
     const size_t smem = (size_t)R * ff * 2 + (size_t)R * (ff / 32) * 4;
     const int grid = gemv_grid((const void*)down_gemv_kernel<R, G, U, GUARD>, smem, d);
-    down_gemv_kernel<R, G, U, GUARD><<<grid, kGemvThreads, smem, st>>>(h, to_ptr(e->w2), ff, d, rw, rs, acc);
+    cudaLaunchConfig_t cfg = {};   // PDL: launch overlaps the SwiGLU GEMV's tail
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kGemvThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, down_gemv_kernel<R, G, U, GUARD>, h, to_ptr(e->w2), ff, d, rw, rs, acc);
     DS_LAUNCH_CHECK("ds_w4_down_gemv");
     return DS_OK;
 }
@@ -409,6 +678,24 @@ extern "C" int ds_w4_swiglu_gemv(const void* x, int R, const ds_w4_expert* e, in
     cudaStream_t st = as_stream(stream);
     const __nv_bfloat16* xb = (const __nv_bfloat16*)x;
     __nv_bfloat16* hb = (__nv_bfloat16*)h;
+    if (G == 128 && k4_use_mma(R)) {
+        constexpr int P = 6;
+        const int NG = d / 128, S = mma_gemv_warps(NG, 2), ngw = (NG + S - 1) / S;
+        const size_t smem = (size_t)S * (mma_gemv_ring_bytes<2, P>() + mma_gemv_aux_bytes(2, ngw));
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(mma_gemv_kernel<2, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            attr = true;
+        }
+        for (int r0 = 0; r0 < R; r0 += kTok) {
+            const int rr = R - r0 < kTok ? R - r0 : kTok;
+            mma_gemv_kernel<2, P><<<ff / 16, 32 * S, smem, st>>>(xb + (size_t)r0 * d, rr, to_ptr(e->w1),
+                                                                 to_ptr(e->w3), d, ff, ngw, hb + (size_t)r0 * ff,
+                                                                 nullptr, 0, nullptr);
+            DS_LAUNCH_CHECK("ds_w4_swiglu_gemv");
+        }
+        return DS_OK;
+    }
     for (int r0 = 0; r0 < R;) {
         const int left = R - r0;
         if (left >= 4) { rc = swiglu_launch<4>(xb + (size_t)r0 * d, e, d, ff, G, hb + (size_t)r0 * ff, st); r0 += 4; }
@@ -426,6 +713,35 @@ extern "C" int ds_w4_down_gemv(const void* h, int R, const ds_w4_expert* e, int 
     DS_CHECK_ARG(e && check_linear(e->w2) && h && route_w && acc, "ds_w4_down_gemv: NULL pointer");
     cudaStream_t st = as_stream(stream);
     const __nv_bfloat16* hb = (const __nv_bfloat16*)h;
+    if (G == 128 && k4_use_mma(R)) {
+        constexpr int P = 8;
+        const int NG = ff / 128, S = mma_gemv_warps(NG, 1), ngw = (NG + S - 1) / S;
+        const size_t smem = (size_t)S * (mma_gemv_ring_bytes<1, P>() + mma_gemv_aux_bytes(1, ngw));
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(mma_gemv_kernel<1, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            attr = true;
+        }
+        for (int r0 = 0; r0 < R; r0 += kTok) {
+            const int rr = R - r0 < kTok ? R - r0 : kTok;
+            // PDL: the down GEMV's weight prologue overlaps the SwiGLU GEMV's tail
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(d / 16);
+            cfg.blockDim = dim3(32 * S);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            cudaLaunchKernelEx(&cfg, mma_gemv_kernel<1, P>, hb + (size_t)r0 * ff, rr, to_ptr(e->w2), to_ptr(e->w2),
+                               ff, d, ngw, (__nv_bfloat16*)nullptr, route_w + (size_t)r0 * route_stride,
+                               route_stride, acc + (size_t)r0 * d);
+            DS_LAUNCH_CHECK("ds_w4_down_gemv");
+        }
+        return DS_OK;
+    }
     for (int r0 = 0; r0 < R;) {
         const int left = R - r0;
         const size_t ho = (size_t)r0 * ff, ao = (size_t)r0 * d;

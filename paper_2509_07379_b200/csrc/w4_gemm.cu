@@ -35,11 +35,14 @@ using namespace sm100;
 
 constexpr int BM = 128;         // weight rows per tile (UMMA M)
 constexpr int BN = 128;         // activation rows per tile (UMMA N)
-constexpr int BK = 64;          // K per stage (one 128-byte swizzle atom of bf16)
+constexpr int BK = 64;          // K per k-tile (one 128-byte swizzle atom of bf16)
 constexpr int UK = 16;          // K per tcgen05.mma (kind::f16)
+constexpr int CK = 2;           // k-tiles per code stage (64 B of codes per weight row)
 constexpr int kMaxExperts = 16;
-constexpr int kThreads = 320;   // 10 warps
-constexpr int kDequantThreads = 256;
+constexpr int kThreads = 608;   // 19 warps
+constexpr int kDequantThreads = 512;   // two groups of 8 warps: even / odd k-tiles
+constexpr int kGroupThreads = 256;
+constexpr int kFirstDequantWarp = 3;
 constexpr int kTileBytes = 128 * 128;  // 128 rows x 128 B
 
 struct W4Mat {
@@ -49,7 +52,7 @@ struct W4Mat {
 };
 
 struct GemmArgs {
-    CUtensorMap codes_map[kMaxExperts][2];   // [N, K/2] u8 tiles {32 B, 128 rows}
+    CUtensorMap codes_map[kMaxExperts][2];   // [N, K/2] u8 tiles {CK * 32 B, 128 rows}
     int K, N, G;
     int kt_per_split;   // k-tiles (of BK) per split
     int splits;
@@ -60,17 +63,26 @@ struct GemmArgs {
     void* out;          // NMAT=2: bf16 H [total_rows, N]; NMAT=1: f32 [splits][total_rows][N]
 };
 
-constexpr int kCodeTile = BM * (BK / 2);   // 128 rows x 32 B of packed codes
-constexpr int kMaxGroupsPerCta = 64;       // staged scales/zeros per row (K-range / G)
+constexpr int kCodeTile = BM * (CK * BK / 2);   // 128 rows x 64 B of packed codes (CK k-tiles)
+constexpr int kMaxGroupsPerCta = 64;            // staged scales/zeros per row (K-range / G)
 
+// Three decoupled rings: packed codes (TMA from HBM, deepest), activation
+// tiles (TMA, L2-resident) and dequantised bf16 weight tiles (written by the
+// dequant warps, read by the tensor cores).
 template <int NMAT>
 struct Smem {
-    static constexpr int STAGES = NMAT == 2 ? 3 : 4;
-    static constexpr int A_BYTES = NMAT * kTileBytes;
-    static constexpr int B_BYTES = BN * 128;
-    static constexpr int C_BYTES = NMAT * kCodeTile;
-    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES + C_BYTES;
-    static constexpr int SC_OFF = STAGES * STAGE_BYTES;                    // bf16 scales [NMAT][128][groups]
+    // dequantised weight stages: >= 3 so the dequant of k-tile kt only waits
+    // for the MMAs of kt - AS (two k-tiles of tensor-core work of slack)
+    static constexpr int AS = NMAT == 2 ? 3 : 4;
+    static constexpr int BS = NMAT == 2 ? 3 : 4;   // activation stages
+    static constexpr int CS = NMAT == 2 ? 2 : 4;   // code stages (CK k-tiles each)
+    static constexpr int A_STAGE = NMAT * kTileBytes;
+    static constexpr int B_STAGE = BN * 128;
+    static constexpr int C_STAGE = NMAT * kCodeTile;
+    static constexpr int A_OFF = 0;
+    static constexpr int B_OFF = A_OFF + AS * A_STAGE;
+    static constexpr int C_OFF = B_OFF + BS * B_STAGE;
+    static constexpr int SC_OFF = C_OFF + CS * C_STAGE;                    // bf16 scales [NMAT][128][groups]
     static constexpr int SC_BYTES = NMAT * BM * kMaxGroupsPerCta * 2;
     static constexpr int Z_OFF = SC_OFF + SC_BYTES;                        // u8 zeros [NMAT][128][groups]
     static constexpr int Z_BYTES = NMAT * BM * kMaxGroupsPerCta;
@@ -107,14 +119,20 @@ template <int NMAT>
 __global__ void __launch_bounds__(kThreads, 1)
 w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constant__ GemmArgs args) {
     using S = Smem<NMAT>;
-    constexpr int STAGES = S::STAGES;
+    constexpr int AS = S::AS, BS = S::BS, CS = S::CS;
     constexpr uint32_t TMEM_COLS = NMAT * BN;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full_b = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
-    uint64_t* full_a = full_b + STAGES;
-    uint64_t* empty = full_a + STAGES;
-    uint64_t* tmem_full = empty + STAGES;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1024-B alignment by offsetting the shared array itself (not via an
+    // integer round trip) so every derived pointer stays in the shared window
+    // and the dequant loads/stores compile to LDS/STS, not generic LD/ST
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint64_t* c_full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
+    uint64_t* c_empty = c_full + CS;
+    uint64_t* b_full = c_empty + CS;
+    uint64_t* b_empty = b_full + BS;
+    uint64_t* a_full = b_empty + BS;
+    uint64_t* a_empty = a_full + AS;
+    uint64_t* tmem_full = a_empty + AS;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
 
     const int e = blockIdx.z;
@@ -127,54 +145,60 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
     const int n0 = nb * BM;
     const int kt0 = split * args.kt_per_split;
     const int KT = args.kt_per_split;
+    const int NCS = (KT + CK - 1) / CK;           // code stages of this CTA
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full_b[s], 1);
-            mbar_init(&full_a[s], kDequantThreads);
-            mbar_init(&empty[s], 1);
-        }
+        for (int s = 0; s < CS; ++s) { mbar_init(&c_full[s], 1); mbar_init(&c_empty[s], kDequantThreads); }
+        for (int s = 0; s < BS; ++s) { mbar_init(&b_full[s], 1); mbar_init(&b_empty[s], 1); }
+        for (int s = 0; s < AS; ++s) { mbar_init(&a_full[s], kGroupThreads); mbar_init(&a_empty[s], 1); }
         mbar_init(tmem_full, 1);
         fence_mbar_init();
         tma_prefetch_desc(&act_map);
         for (int j = 0; j < NMAT; ++j) tma_prefetch_desc(&args.codes_map[e][j]);
     }
-    if (warp == 1) tmem_alloc<TMEM_COLS>(tmem_slot);
+    if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
-        // ---------------------------------------------------- TMA producer
+        // ---------------------------------------------- code producer (HBM)
         if (lane == 0) {
-            const int row_coord = args.row_start[e] + m0;
-            for (int kt = 0; kt < KT; ++kt) {
-                const int s = kt % STAGES;
-                if (kt >= STAGES) mbar_wait(&empty[s], ((kt / STAGES) - 1) & 1);
-                uint8_t* b_tile = smem + s * S::STAGE_BYTES + S::A_BYTES;
-                uint8_t* c_tile = b_tile + S::B_BYTES;
-                mbar_expect_tx(&full_b[s], S::B_BYTES + S::C_BYTES);
-                tma_load_2d(b_tile, &act_map, &full_b[s], (kt0 + kt) * BK, row_coord);
+            for (int j = 0; j < NCS; ++j) {
+                const int s = j % CS;
+                if (j >= CS) mbar_wait(&c_empty[s], ((j / CS) - 1) & 1);
+                uint8_t* c_tile = smem + S::C_OFF + s * S::C_STAGE;
+                mbar_expect_tx(&c_full[s], S::C_STAGE);
 #pragma unroll
-                for (int j = 0; j < NMAT; ++j)
-                    tma_load_2d(c_tile + j * kCodeTile, &args.codes_map[e][j], &full_b[s], (kt0 + kt) * (BK / 2), n0);
+                for (int m = 0; m < NMAT; ++m)
+                    tma_load_2d(c_tile + m * kCodeTile, &args.codes_map[e][m], &c_full[s],
+                                (kt0 + j * CK) * (BK / 2), n0);
             }
         }
     } else if (warp == 1) {
+        // ----------------------------------------- activation producer (L2)
+        if (lane == 0) {
+            const int row_coord = args.row_start[e] + m0;
+            for (int kt = 0; kt < KT; ++kt) {
+                const int s = kt % BS;
+                if (kt >= BS) mbar_wait(&b_empty[s], ((kt / BS) - 1) & 1);
+                mbar_expect_tx(&b_full[s], S::B_STAGE);
+                tma_load_2d(smem + S::B_OFF + s * S::B_STAGE, &act_map, &b_full[s], (kt0 + kt) * BK, row_coord);
+            }
+        }
+    } else if (warp == 2) {
         // -------------------------------------------------------- MMA issuer
         if (lane == 0) {
             const uint32_t idesc = idesc_bf16_f32(BM, BN);
             for (int kt = 0; kt < KT; ++kt) {
-                const int s = kt % STAGES;
-                const uint32_t ph = (kt / STAGES) & 1;
-                mbar_wait(&full_b[s], ph);
-                mbar_wait(&full_a[s], ph);
+                const int sa = kt % AS, sb = kt % BS;
+                mbar_wait(&b_full[sb], (kt / BS) & 1);
+                mbar_wait(&a_full[sa], (kt / AS) & 1);
                 tc_fence_after();
-                const uint32_t a_addr = smem_u32(smem + s * S::STAGE_BYTES);
-                const uint32_t b_addr = a_addr + S::A_BYTES;
-                const uint64_t bdesc = umma_desc_sw128(b_addr);
+                const uint32_t a_addr = smem_u32(smem + S::A_OFF + sa * S::A_STAGE);
+                const uint64_t bdesc = umma_desc_sw128(smem_u32(smem + S::B_OFF + sb * S::B_STAGE));
 #pragma unroll
                 for (int kk = 0; kk < BK / UK; ++kk) {
 #pragma unroll
@@ -185,23 +209,27 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
                                  (kt | kk) != 0);
                     }
                 }
-                mma_commit(&empty[s]);
+                mma_commit(&a_empty[sa]);
+                mma_commit(&b_empty[sb]);
             }
             mma_commit(tmem_full);
         }
     } else {
         // ------------------------------------------------ dequant producers
-        const int t = threadIdx.x - 64;          // 0..255
+        const int td = threadIdx.x - 32 * kFirstDequantWarp;  // 0..511
+        const int dg = td >> 8;                  // dequant group: k-tiles kt = 2i + dg (CK = 2)
+        const int t = td & 255;
         const int nl = t >> 1, half = t & 1;     // 2 threads per weight row (32 codes each)
         const int K = args.K, G = args.G;
         const int gpr = K / G;
         const int g0 = kt0 * BK / G;             // first group touching this CTA's k-range
         const int ng = ((kt0 + KT) * BK + G - 1) / G - g0;   // groups touched (<= kMaxGroupsPerCta)
+        const int gshift = G == 128 ? 7 : 6;                 // G is 64 or 128 (checked on the host)
         const W4Mat* W = args.w[e];
         uint16_t* sc_s = reinterpret_cast<uint16_t*>(smem + S::SC_OFF);
         uint8_t* z_s = smem + S::Z_OFF;
         // stage the n-block's scales and zeros for the whole k-range once
-        for (int i = t; i < NMAT * BM * ng; i += kDequantThreads) {
+        for (int i = td; i < NMAT * BM * ng; i += kDequantThreads) {
             const int j = i / (BM * ng), rem = i - j * BM * ng, r = rem / ng, g = rem - r * ng;
             const size_t gi = (size_t)(n0 + r) * gpr + g0 + g;
             sc_s[(j * BM + r) * kMaxGroupsPerCta + g] = __ldg(W[j].scales + gi);
@@ -209,26 +237,33 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kDequantThreads));
         const int swz = nl & 7;
-        for (int kt = 0; kt < KT; ++kt) {
-            const int s = kt % STAGES;
-            mbar_wait(&full_b[s], (kt / STAGES) & 1);            // codes (and B) landed
-            uint8_t* stage = smem + s * S::STAGE_BYTES;
-            const uint8_t* c_tile = stage + S::A_BYTES + S::B_BYTES;
-            const int g = ((kt0 + kt) * BK + 32 * half) / G - g0;
+        static_assert(CK == 2, "two dequant groups alternate over the 2 k-tiles of a code stage");
+        for (int cj = 0; cj < NCS; ++cj) {
+            const int kt = cj * CK + dg, cs = cj % CS;
+            if (kt < KT) {
+                const int sa = kt % AS;
+                mbar_wait(&c_full[cs], (cj / CS) & 1);                           // codes landed
+                if (kt >= AS) mbar_wait(&a_empty[sa], ((kt / AS) - 1) & 1);      // tensor cores done with A[sa]
+                uint8_t* a_tile = smem + S::A_OFF + sa * S::A_STAGE;
+                const uint8_t* c_tile = smem + S::C_OFF + cs * S::C_STAGE;
+                const int g = (((kt0 + kt) * BK + 32 * half) >> gshift) - g0;
 #pragma unroll
-            for (int j = 0; j < NMAT; ++j) {
-                const uint4 c = *reinterpret_cast<const uint4*>(c_tile + j * kCodeTile + nl * 32 + half * 16);
-                const uint32_t z = z_s[(j * BM + nl) * kMaxGroupsPerCta + g];
-                const uint32_t zz = (0x4300u | z) * 0x00010001u;
-                const uint32_t ss = (uint32_t)sc_s[(j * BM + nl) * kMaxGroupsPerCta + g] * 0x00010001u;
-                dequant32(c, zz, ss, stage + j * kTileBytes + nl * 128, 4 * half, swz);
+                for (int j = 0; j < NMAT; ++j) {
+                    const uint4 c = *reinterpret_cast<const uint4*>(c_tile + j * kCodeTile + nl * (CK * 32) +
+                                                                    dg * 32 + half * 16);
+                    const uint32_t z = z_s[(j * BM + nl) * kMaxGroupsPerCta + g];
+                    const uint32_t zz = (0x4300u | z) * 0x00010001u;
+                    const uint32_t ss = (uint32_t)sc_s[(j * BM + nl) * kMaxGroupsPerCta + g] * 0x00010001u;
+                    dequant32(c, zz, ss, a_tile + j * kTileBytes + nl * 128, 4 * half, swz);
+                }
+                fence_proxy_async_smem();
+                mbar_arrive(&a_full[sa]);
             }
-            fence_proxy_async_smem();
-            mbar_arrive(&full_a[s]);
+            mbar_arrive(&c_empty[cs]);           // both groups release every code stage
         }
 
         // ---------------------------------------------------------- epilogue
-        if (warp < 6) {
+        if (warp < kFirstDequantWarp + 4) {
             const int q = warp & 3;                   // TMEM lane quadrant of this warp
             const int nrow = n0 + 32 * q + lane;
             mbar_wait(tmem_full, 0);
@@ -264,7 +299,7 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) {
+    if (warp == 2) {
         tc_fence_after();
         tmem_dealloc<TMEM_COLS>(tmem_base);
     }
@@ -303,7 +338,7 @@ int make_codes_map(CUtensorMap* map, const void* codes, int N, int K) {
     if (!fn) return fail(DS_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
     cuuint64_t dims[2] = {(cuuint64_t)K / 2, (cuuint64_t)N};
     cuuint64_t strides[1] = {(cuuint64_t)K / 2};
-    cuuint32_t box[2] = {BK / 2, BM};
+    cuuint32_t box[2] = {CK * BK / 2, BM};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(codes), dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

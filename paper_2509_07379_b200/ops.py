@@ -79,16 +79,24 @@ def unpermute_partial(y: torch.Tensor, pos, w, idx, owned_mask: int, out: torch.
     _count("ds_unpermute_partial")
 
 
+def _gemv_passes(R: int, G: int) -> int:
+    """kernel launches of one K4 call: the mma.sync GEMV (G = 128, R >= 2) takes
+    8 rows per pass, the FHFMA GEMV 4/2/1 (csrc/w4.cu k4_use_mma)."""
+    if G == 128 and R >= 2:
+        return (R + 7) // 8
+    return R // 4 + (R % 4) // 2 + (R % 2)
+
+
 def swiglu_gemv(x: torch.Tensor, e: _lib.W4Expert, d: int, ff: int, G: int, h: torch.Tensor) -> None:
     _lib.call("ds_w4_swiglu_gemv", ptr(x), x.shape[0], C.byref(e), d, ff, G, ptr(h), stream_ptr())
-    _count("ds_w4_swiglu_gemv", (x.shape[0] + 3) // 4)
+    _count("ds_w4_swiglu_gemv", _gemv_passes(x.shape[0], G))
 
 
 def down_gemv(h: torch.Tensor, e: _lib.W4Expert, d: int, ff: int, G: int, route_w: torch.Tensor,
               route_stride: int, acc: torch.Tensor) -> None:
     _lib.call("ds_w4_down_gemv", ptr(h), h.shape[0], C.byref(e), d, ff, G, ptr(route_w), route_stride, ptr(acc),
               stream_ptr())
-    _count("ds_w4_down_gemv", (h.shape[0] + 3) // 4)
+    _count("ds_w4_down_gemv", _gemv_passes(h.shape[0], G))
 
 
 def combine_finalize(acc: torch.Tensor, resid: torch.Tensor, out: torch.Tensor) -> None:

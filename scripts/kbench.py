@@ -58,6 +58,10 @@ if "k4" in only:
     bytes2 = d * ff // 2 + d * (ff // G) * 2 + d * (ff // G) // 2
     res["k4_swiglu"] = {"us": t1 * 1e6, "GBs": bytes13 / t1 / 1e9, "frac": bytes13 / t1 / 1e9 / peaks["hbm_gbs"]}
     res["k4_down"] = {"us": t2 * 1e6, "GBs": bytes2 / t2 / 1e9, "frac": bytes2 / t2 / 1e9 / peaks["hbm_gbs"]}
+    # the roofline unit of bench.py: one expert = SwiGLU GEMV + down GEMV back to back
+    t12 = timeit(lambda i: (ops.swiglu_gemv(x, es[i % NB], d, ff, G, h),
+                            ops.down_gemv(h, es[i % NB], d, ff, G, rw, 1, acc)), a.iters)
+    res["k4_expert"] = {"us": t12 * 1e6, "GBs": total / t12 / 1e9, "frac": total / t12 / 1e9 / peaks["hbm_gbs"]}
 if "k3" in only:
     R = a.rows
     xp = (torch.randn(R, d, device=dev)).to(torch.bfloat16)

@@ -120,13 +120,14 @@ def test_w4_dequant_bit_exact(cuda):
         assert np.array_equal(_bf16_bits(out), WR.dequant(c, s, z, K, N, G))
 
 
-@pytest.mark.parametrize("d,ff,R", [(256, 896, 1), (4096, 14336, 1), (4096, 14336, 3), (6144, 16384, 1),
-                                    (256, 896, 6)])
-def test_w4_gemv_vs_f64_reference(d, ff, R, cuda):
-    """K4 decode GEMV.  It factorises the group scale out of the dot product,
-    so its reference weights are the EXACT (q - z) * s (oracle.w4_ref.dequant_exact);
-    against those the only error is f32 accumulation."""
-    G = 128
+@pytest.mark.parametrize("d,ff,R,G", [(256, 896, 1, 128), (4096, 14336, 1, 128), (4096, 14336, 3, 128),
+                                      (6144, 16384, 1, 128), (256, 896, 6, 128), (4096, 14336, 8, 128),
+                                      (256, 896, 11, 128), (512, 1024, 3, 64), (256, 896, 5, 64)])
+def test_w4_gemv_vs_f64_reference(d, ff, R, G, cuda):
+    """K4 decode GEMV (G = 128: v3, mma.sync; G = 64: v2, FHFMA).  Both factorise
+    the group scale out of the dot product, so the reference weights are the
+    EXACT (q - z) * s (oracle.w4_ref.dequant_exact); against those the only
+    error is f32 accumulation.  R = 11 crosses the 8-row pass boundary."""
     offs, total = _layout(d, ff, G)
     blob = torch.zeros(total, dtype=torch.uint8, device=cuda)
     _lib.call("ds_w4_generate", 77, 2, 3, d, ff, G, _lib.ptr(blob), _lib.stream_ptr())
