@@ -242,8 +242,14 @@ class _State:
     """Mutable per-request simulation state: stream clocks, cache, log."""
 
     def __init__(self, policy: SchedulerPolicy, cfg: ModelConfig, cost: CostModel,
-                 prefill_non_moe_s: float | None = None):
+                 prefill_non_moe_s: float | None = None, cancel_chunk_bytes: int | None = None):
         self.policy, self.cfg, self.cost = policy, cfg, cost
+        # B200 extension (engine.LinkQueue): a prefetch the gate proves wrong is
+        # cancelled after its in-flight chunk instead of completing (SPEC.md:429
+        # models no cancellation; None keeps the SPEC semantics)
+        self.cancel_ns = None if cancel_chunk_bytes is None else _ns(
+            cost.link_latency_s + min(cancel_chunk_bytes, cfg.expert_bytes) / cost.link_bandwidth_bytes_per_s)
+        self.lazy: list = []           # cancel mode: (expert, earliest start) of the next layer's prefetch
         self.tl = EventTimeline()
         self.cache = DeviceExpertCache(slot_count(policy, cfg))
         self.t_compute = 0
@@ -365,6 +371,8 @@ def schedule_decode_layer(st: _State, t: int, l: int, E: tuple, P_next: tuple | 
         ready = {e: st.transfer((l, e), g, "transfer", **kw) for e in E}
         rec = {"phase": "decode", "token": t, "layer": l, "fetch": list(E), "kind": "ondemand"}
     else:
+        if st.cancel_ns is not None:
+            _place_cancellable(st, l, E, g, kw)
         pf = st.pending
         P = tuple(sorted(pf))
         hit = [e for e in E if e in pf]
@@ -391,9 +399,42 @@ def schedule_decode_layer(st: _State, t: int, l: int, E: tuple, P_next: tuple | 
         p1 = p0 + (st.pred if pred_ready is None else pred_ready)
         st.tl.add("predict", "predict", p0, p1, layer=l + 1, **kw)
         st.t_predict = p1
-        for e in sorted(P_next):
-            st.pending[e] = st.transfer((l + 1, e), p1, "transfer", **kw)
+        if st.cancel_ns is not None:
+            st.lazy = [(e, p1) for e in sorted(P_next)]      # placed at the next gate
+        else:
+            for e in sorted(P_next):
+                st.pending[e] = st.transfer((l + 1, e), p1, "transfer", **kw)
     return rec
+
+
+def _place_cancellable(st: _State, l: int, E: tuple, g: int, kw: dict) -> None:
+    """Place layer l's prefetches on the link knowing the gate time g: a
+    correct one runs to completion; a wrong one stops one chunk after the gate
+    (or never starts if the link reached it only after the gate)."""
+    st.pending = {}
+    taken: set = set()
+    for e, earliest in st.lazy:
+        c = st.cache
+        slot = min((i for i in range(c.slot_count) if i not in taken), key=lambda i: (c.free_at[i], i))
+        free = c.free_at[slot]
+        taken.add(slot)
+        start = max(st.t_link, earliest, free)
+        if e in E:
+            end = start + st.T
+            kind = "transfer"
+        elif start >= g:
+            st.pending[e] = (slot, start)          # never issued: its slot takes the re-fetch
+            continue
+        else:
+            end = min(start + st.T, g + st.cancel_ns)
+            kind = "cancelled"
+        st.tl.add("comm", kind, start, end, expert=e, layer=l, **kw)
+        st.cache.load(slot, (l, e), start, end)
+        st.t_link = end
+        st.link_busy += end - start
+        st.link_bytes += int(round(st.cfg.expert_bytes * (end - start) / st.T))
+        st.pending[e] = (slot, end)
+    st.lazy = []
 
 
 def _requests(traces) -> list:
@@ -410,7 +451,8 @@ def _requests(traces) -> list:
 
 
 def simulate_request(policy, traces, cfg: ModelConfig, cost: CostModel, net=None, pop=None, aff=None,
-                     seed: int = 0, check: bool = True, prefill_non_moe_s: float | None = None):
+                     seed: int = 0, check: bool = True, prefill_non_moe_s: float | None = None,
+                     cancel_chunk_bytes: int | None = None):
     """Simulate one request (its prefill + decode traces) under a policy.
 
     net: a predictor object with ``predict(trace, l) -> tuple`` (the
@@ -418,6 +460,8 @@ def simulate_request(policy, traces, cfg: ModelConfig, cost: CostModel, net=None
     ``oracle`` predicts the true selection with zero prediction latency.
     prefill_non_moe_s: optional non-MoE time of a prefill layer (B200
     calibration; default: cost.non_moe_compute_per_layer_s as in the SPEC).
+    cancel_chunk_bytes: model the B200 runtime's cancellable chunked prefetch
+    (a wrong prefetch stops one chunk after the gate); None = SPEC semantics.
     Returns (RequestMetrics, EventTimeline, cache log)."""
     pol = SchedulerPolicy(policy)
     traces = list(traces)
@@ -437,7 +481,7 @@ def simulate_request(policy, traces, cfg: ModelConfig, cost: CostModel, net=None
             raise ConfigError("policy duoserve needs a predictor")
         if hasattr(net, "input_dim") and not hasattr(net, "predict"):
             raise ConfigError("pass a predictor object (MLPPredictor / PrecomputedPredictor), not a raw network")
-    st = _State(pol, cfg, cost, prefill_non_moe_s)
+    st = _State(pol, cfg, cost, prefill_non_moe_s, cancel_chunk_bytes)
     for l in range(L):
         act: dict = {}
         for tr in pre:

@@ -70,12 +70,19 @@ offs, blob = ops.expert_layout(d, ff, G)
 host = torch.empty(blob, dtype=torch.uint8).pin_memory()
 dst = torch.empty(blob, dtype=torch.uint8, device=dev)
 cs = torch.cuda.Stream()
+def copies(n, src, dst_):
+    def f(i):
+        for _ in range(n):
+            dst_.copy_(src, non_blocking=True)
+    return f
+
+
 with torch.cuda.stream(cs):
-    t_blob = timeit(lambda i: dst.copy_(host, non_blocking=True), flush_l2=False, stream=cs)
+    t_blob = timeit(copies(8, host, dst), iters=5, flush_l2=False, stream=cs) / 8   # back to back, like the link
     small_h = torch.empty(4096, dtype=torch.uint8).pin_memory()
     small_d = torch.empty(4096, dtype=torch.uint8, device=dev)
-    t_small = timeit(lambda i: small_d.copy_(small_h, non_blocking=True), iters=50, flush_l2=False, stream=cs)
-bw = blob / max(t_blob - t_small, 1e-9)
+    t_small = timeit(copies(1, small_h, small_d), iters=50, flush_l2=False, stream=cs)
+bw = blob / t_blob
 res["link"] = {"blob_bytes": blob, "blob_us": t_blob * 1e6, "small_us": t_small * 1e6, "GBs": bw / 1e9}
 del host
 
@@ -85,7 +92,8 @@ P = a.prefill
 kv = KVCache(sh, P + a.decode + 8, dev)
 cos, sin = rope_tables(sh, P + a.decode + 8, dev)
 hp = (torch.randn(P, d, device=dev) * 0.5).to(torch.bfloat16)
-t_attn_p = timeit(lambda i: attention_block(sh, W.layers[0], hp, kv, 0, 0, cos, sin))
+# eager prefill attention, back to back (the engine issues it eagerly too)
+t_attn_p = timeit(lambda i: [attention_block(sh, W.layers[0], hp, kv, 0, 0, cos, sin) for _ in range(4)]) / 4
 h1 = hp[:1].clone()
 t_attn_d = timeit(lambda i: attention_block(sh, W.layers[0], h1, kv, 0, P, cos, sin))
 idx = torch.empty(P, k, dtype=torch.int32, device=dev)
@@ -165,6 +173,19 @@ for rep in range(2):
     torch.cuda.synchronize()
     meas.append({"ttft_ms": e0.elapsed_time(e1), "decode_ms_per_token": e1.elapsed_time(e2) / a.decode})
 m = meas[-1]
+# decode non-MoE + gate as the engine runs it: the per-layer CUDA graph replay
+if getattr(eng, "g_graphs", None):
+    gr = eng.g_graphs[1]
+    t_graph = timeit(lambda i: [gr.replay() for _ in range(8)], flush_l2=False) / 8
+    res["non_moe"]["decode_graph_us"] = t_graph * 1e6
+    cost = C.CostModel(link_bandwidth_bytes_per_s=cost.link_bandwidth_bytes_per_s,
+                       link_latency_s=cost.link_latency_s, expert_compute_base_s=cost.expert_compute_base_s,
+                       expert_compute_per_token_s=cost.expert_compute_per_token_s,
+                       non_moe_compute_per_layer_s=max(t_graph - t_gate, 1e-7), gate_compute_s=t_gate,
+                       predictor_latency_s=cost.predictor_latency_s)
+    preset = json.loads(C.config_to_json(cfg, cost))
+    preset["model"]["name"] = f"{sh.name}-b200"
+    res["preset"] = preset
 traces = [T.ActivationTrace(0, "prefill", t, tuple(tuple(int(e) for e in eng.paths_prefill[t, l]) for l in range(L)))
           for t in range(P)]
 traces += [T.ActivationTrace(0, "decode", P + t, tuple(tuple(sorted(p)) for p in path))
@@ -175,11 +196,15 @@ for r in eng.log:
         table[(0, P + r["token"], r["layer"])] = tuple(r["pred"])
 pp = PrecomputedPredictor(table)
 sim = {}
-for pol in ("duoserve", "oracle", "ondemand", "prefetchall"):
-    mm, _, log = S.simulate_request(pol, traces, cfg, cost, net=pp, prefill_non_moe_s=res["prefill_non_moe_s"])
+# the runtime's cancellation: depth x speculative chunk still in flight after the gate
+cancel = eng.link.depth * eng.link.spec_chunk
+for pol in ("duoserve", "duoserve+cancel", "oracle", "ondemand", "prefetchall"):
+    mm, _, log = S.simulate_request(pol.split("+")[0], traces, cfg, cost, net=pp,
+                                    prefill_non_moe_s=res["prefill_non_moe_s"],
+                                    cancel_chunk_bytes=cancel if pol.endswith("+cancel") else None)
     sim[pol] = {"ttft_ms": mm.ttft_s * 1e3, "decode_ms_per_token": (mm.e2e_s - mm.ttft_s) * 1e3 / a.decode,
                 "refetch_count": mm.refetch_count, "link_bytes": mm.link_bytes}
-    if pol == "duoserve":
+    if pol.startswith("duoserve"):
         rt = [dict(r, token=P + r["token"]) if "token" in r else r for r in eng.log]
         sim[pol]["log_equals_runtime"] = log == rt
 res["request"] = {"measured": m, "simulated": sim, "prefill": P, "decode": a.decode}

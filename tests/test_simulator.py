@@ -209,3 +209,24 @@ def test_run_experiment_deterministic_and_ordered():
         assert rd.e2e_s < ro.e2e_s and rd.e2e_s < rp.e2e_s
     with pytest.raises(T.TraceError):
         S.run_experiment(["ondemand"], T.TraceDataset("fixture", 6, 8, 2, []), cfg, cost)
+
+
+def test_cancellable_prefetch_extension():
+    """B200 extension: with chunked cancellation a wrong prefetch stops one
+    chunk after the gate, so decode is never slower than the SPEC schedule,
+    the decisions (cache log) are unchanged, and with perfect predictions the
+    two schedules coincide."""
+    ds, cfg = _dataset(n=6, seed=4)
+    cost = _cost(10, 2, nm_ms=1)
+    pp = PopularityPredictor(ST.build_popularity(ds), cfg.top_k)
+    chunk = cfg.expert_bytes // 8
+    for rid, trs in ds.by_request().items():
+        ms, tls, ls = S.simulate_request("duoserve", trs, cfg, cost, net=pp)
+        mc, tlc, lc = S.simulate_request("duoserve", trs, cfg, cost, net=pp, cancel_chunk_bytes=chunk)
+        assert lc == ls
+        assert mc.e2e_s <= ms.e2e_s and mc.ttft_s == ms.ttft_s
+        assert mc.link_bytes <= ms.link_bytes
+        tlc.check()
+        mo, _, _ = S.simulate_request("oracle", trs, cfg, cost)
+        mo2, _, _ = S.simulate_request("oracle", trs, cfg, cost, cancel_chunk_bytes=chunk)
+        assert mo2.e2e_s == mo.e2e_s
