@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--ep", action="store_true",
                     help="under torchrun: expert parallelism (rank r owns experts e %% N == r, per-rank pinned "
                          "shard + cache, NCCL all-reduce combine) on ONE request instead of N replicas")
+    ap.add_argument("--ep-combine", default="allreduce", choices=["allreduce", "alltoall"],
+                    help="--ep combine collective: one all-reduce, or all_to_all_single + all-gather")
     ap.add_argument("--out", default=None, help="also write the JSON line to this file")
     return ap.parse_args()
 
@@ -264,7 +266,7 @@ def run_ours(args):
     ep = None
     if args.ep and ws > 1:
         from paper_2509_07379_b200.ep import EPConfig
-        ep = EPConfig(rank, ws)
+        ep = EPConfig(rank, ws, combine=args.ep_combine)
     eng = Engine(shape, args.policy if args.policy != "oracle" else "duoserve", seed=args.seed, device=dev,
                  predictor=net, pop=pop, aff=aff, max_seq=args.prefill + args.decode + 8,
                  max_prefill=args.prefill, cancel_mispredicted=not args.no_cancel, chunk_mb=args.chunk_mb,
@@ -367,7 +369,7 @@ def run_ours(args):
                                f"1 request per GPU, policy {args.policy}"
                                f"{'' if args.no_cancel else ' + chunked cancellable prefetch'}",
                    "model": shape.name, "global_batch": 1 if ep else ws, "seq_len": args.prefill + args.decode,
-                   "parallelism": (f"ep{ws}" if ep else f"replicas{ws}") if ws > 1 else "single-gpu",
+                   "parallelism": (f"ep{ws}-{ep.combine}" if ep else f"replicas{ws}") if ws > 1 else "single-gpu",
                    "expert_slots": eng.n_slots,
                    "l2": "inputs > L2: every expert byte is streamed from pinned host memory per request"},
         "ttft_ms": round(ttft, 2), "decode_tok_s": round(args.decode / (dec_ms / 1e3), 3),

@@ -623,7 +623,7 @@ class Engine:
         else:
             part = self.p_part[:T]
             ops.unpermute_partial(self.p_y[:T * self.k], self.p_pos[:T * self.k], w, idx, self.owner_bits, part)
-            self.ep.all_reduce_(part)                       # sum of the ranks' expert terms
+            self.ep.combine_(part)                          # sum of the ranks' expert terms
             ops.combine_finalize(part, h, out)
         return out
 
@@ -724,7 +724,7 @@ class Engine:
         if out is None:
             out = torch.empty_like(h)
         if self.ep is not None:
-            self.ep.all_reduce_(self.acc)                      # sum of the ranks' expert terms
+            self.ep.combine_(self.acc)                         # sum of the ranks' expert terms
         ops.combine_finalize(self.acc, h, out)
         return out
 

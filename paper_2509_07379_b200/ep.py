@@ -6,8 +6,12 @@ own copy stream / link, so the aggregate host-link bandwidth grows with G.
 Attention, norms and the gate stay replicated (batch-1 serving: every rank
 sees the same tokens, and the deterministic kernels give the same routing on
 every rank).  Each rank computes the routing-weighted sum of ITS selected
-experts into an f32 partial [T, d]; one all-reduce (NCCL over NVLink on B200;
-gloo in the CPU tests) combines them.  With top-k = 2 at most two ranks hold a
+experts into an f32 partial [T, d]; one collective (NCCL over NVLink on B200;
+gloo in the CPU tests) combines them — `combine="allreduce"` (one all-reduce)
+or `combine="alltoall"` (the north star's all-to-all exchange: each rank
+receives every rank's share of one 1/G slice of the partial through
+all_to_all_single, sums the G contributions in rank order and the slices are
+all-gathered back, i.e. reduce-scatter + all-gather spelt with all-to-all).  With top-k = 2 at most two ranks hold a
 non-zero term per element and adding exact zeros is exact, so the EP result is
 bit-identical to the single-GPU result (tests/test_ep.py).
 
@@ -61,13 +65,52 @@ class EPConfig:
     rank: int
     world: int
     group: object = None          # torch.distributed ProcessGroup (None = default group)
+    combine: str = "allreduce"    # "allreduce" | "alltoall"
 
     @classmethod
-    def from_env(cls) -> "EPConfig | None":
+    def from_env(cls, combine: str = "allreduce") -> "EPConfig | None":
         import torch.distributed as dist
         if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
             return None
-        return cls(dist.get_rank(), dist.get_world_size(), None)
+        return cls(dist.get_rank(), dist.get_world_size(), None, combine)
+
+    def combine_(self, t: torch.Tensor) -> torch.Tensor:
+        """In-place sum of the ranks' partials with the configured collective."""
+        if self.combine == "alltoall":
+            return self.all_to_all_combine_(t)
+        if self.combine != "allreduce":
+            raise ValueError(f"unknown EP combine {self.combine!r}")
+        return self.all_reduce_(t)
+
+    def all_to_all_combine_(self, t: torch.Tensor) -> torch.Tensor:
+        """Sum of the ranks' partials via all-to-all: slice j of every rank's
+        partial goes to rank j, which adds the G slices in rank order, then the
+        summed slices are all-gathered.  Per element at most k ranks hold a
+        non-zero term, so this equals the all-reduce bit for bit."""
+        import torch.distributed as dist
+        G = self.world
+        flat = t.reshape(-1)
+        n = flat.numel()
+        c = (n + G - 1) // G
+        dev = t.device
+        stage = t.is_cuda and dist.get_backend(self.group) == "gloo"
+        send = torch.zeros(G * c, dtype=t.dtype, device="cpu" if stage else dev)
+        send[:n].copy_(flat)
+        recv = torch.empty_like(send)
+        dist.all_to_all_single(recv, send, group=self.group)
+        parts = recv.view(G, c)
+        mine = parts[0].clone()
+        for j in range(1, G):
+            mine += parts[j]
+        if dist.get_backend(self.group) == "gloo":
+            chunks = [torch.empty_like(mine) for _ in range(G)]
+            dist.all_gather(chunks, mine, group=self.group)
+            out = torch.cat(chunks)
+        else:
+            out = torch.empty(G * c, dtype=t.dtype, device=mine.device)
+            dist.all_gather_into_tensor(out, mine, group=self.group)
+        flat.copy_(out[:n])
+        return t
 
     def all_reduce_(self, t: torch.Tensor) -> torch.Tensor:
         """In-place SUM all-reduce (NCCL over NVLink for CUDA tensors; a gloo

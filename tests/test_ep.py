@@ -61,15 +61,17 @@ def _worker(rank, world, port, q):
     for j in range(k):
         own = torch.tensor([cfg.owns(int(e)) for e in idx[:, j]])
         part = part + torch.where(own[:, None], w[:, j:j + 1] * y[pos[:, j]], torch.zeros(()))
+    part2 = part.clone()
     cfg.all_reduce_(part)
+    cfg.all_to_all_combine_(part2)
     full = torch.zeros((T, d))
     for j in range(k):
         full = full + w[:, j:j + 1] * y[pos[:, j]]
-    q.put((rank, bool(torch.equal(part, full))))
+    q.put((rank, bool(torch.equal(part, full)) and bool(torch.equal(part2, full))))
     dist.destroy_process_group()
 
 
-def test_all_reduce_combine_bit_identical_world2():
+def test_all_reduce_and_all_to_all_combine_bit_identical_world2():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()

@@ -27,7 +27,7 @@ def _setup(dev):
     return shape, net, pop, aff, dense, ids
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, combine="allreduce"):
     import torch.distributed as dist
     from paper_2509_07379_b200.engine import Engine
     from paper_2509_07379_b200.ep import EPConfig
@@ -36,14 +36,15 @@ def _worker(rank, world, port, q):
     dev = torch.device("cuda:0")
     shape, net, pop, aff, dense, ids = _setup(dev)
     eng = Engine(shape, "duoserve", seed=3, dense=dense, predictor=net, pop=pop, aff=aff, max_seq=64,
-                 max_prefill=PREFILL, ep=EPConfig(rank, world))
+                 max_prefill=PREFILL, ep=EPConfig(rank, world, combine=combine))
     toks = eng.generate(ids, DECODE)
     q.put((rank, toks, eng.log, [list(map(list, p)) for p in eng.paths_decode], eng.paths_prefill.tolist(),
            eng.store.experts))
     dist.destroy_process_group()
 
 
-def test_ep_world2_matches_single_gpu(cuda):
+@pytest.mark.parametrize("combine", ["allreduce", "alltoall"])
+def test_ep_world2_matches_single_gpu(cuda, combine):
     from oracle import predictor_ref, sim_ref
     from paper_2509_07379_b200.engine import Engine
     shape, net, pop, aff, dense, ids = _setup(cuda)
@@ -56,7 +57,7 @@ def test_ep_world2_matches_single_gpu(cuda):
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, combine)) for r in range(2)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=600) for _ in procs], key=lambda r: r[0])
