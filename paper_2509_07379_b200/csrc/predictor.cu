@@ -24,6 +24,7 @@
 #include "ds_common.cuh"
 
 #include <cooperative_groups.h>
+#include <cstdlib>
 #include <vector>
 
 namespace ds {
@@ -426,7 +427,11 @@ int run_forward(const ds_mlp_desc* d, const double* packed, const StateArgs* s, 
             attr_set = true;
         }
         if (smem > 200 * 1024) return fail(DS_ERR_UNSUPPORTED, "ds_predictor: layer too wide");
+        // CTAs of the persistent kernel (one per SM by default); DS_K5_CTAS caps it
+        // (A/B: fewer SMs leave room for the decode GEMV it overlaps with)
+        static const int cap = getenv("DS_K5_CTAS") ? atoi(getenv("DS_K5_CTAS")) : 0;
         int grid = num_sms();
+        if (cap > 0 && cap < grid) grid = cap;
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mlp_fused_kernel, kFusedThreads, smem);
         if (per_sm < 1) return fail(DS_ERR_UNSUPPORTED, "ds_predictor: fused kernel cannot be resident");

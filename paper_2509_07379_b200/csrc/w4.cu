@@ -526,9 +526,18 @@ int gemv_grid(const void* fn, size_t smem, int rows_needed) {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kGemvThreads, smem);
     if (per_sm < 1) per_sm = 1;
+    const int wpc = kGemvThreads / 32;
     int grid = per_sm * num_sms();
-    int need = (rows_needed + (kGemvThreads / 32) - 1) / (kGemvThreads / 32);
-    return grid < need ? grid : need;
+    int need = (rows_needed + wpc - 1) / wpc;
+    if (grid >= need) return need;
+    // rows pass over the resident warps `passes` times; shrink the grid so every
+    // warp runs exactly that many rows (no last pass carried by a few warps)
+    static const bool balance = getenv("DS_K4_NO_BALANCE") == nullptr;
+    if (balance) {
+        const int passes = (rows_needed + grid * wpc - 1) / (grid * wpc);
+        grid = (rows_needed + passes * wpc - 1) / (passes * wpc);
+    }
+    return grid;
 }
 
 bool check_linear(const ds_w4_linear& l) { return l.codes && l.scales && l.zeros; }

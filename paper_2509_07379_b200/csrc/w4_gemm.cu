@@ -61,6 +61,11 @@ struct GemmArgs {
     int rows[kMaxExperts];
     W4Mat w[kMaxExperts][2];
     void* out;          // NMAT=2: bf16 H [total_rows, N]; NMAT=1: f32 [splits][total_rows][N]
+    // runtime shared-memory layout after the fixed A / B rings: as many code
+    // stages as fit once the scales / zeros of this launch's k-range are staged
+    int code_stages;    // CS
+    int ng_stride;      // staged groups per weight row
+    int sc_off, z_off, bar_off, smem_bytes;
 };
 
 constexpr int kCodeTile = BM * (CK * BK / 2);   // 128 rows x 64 B of packed codes (CK k-tiles)
@@ -75,20 +80,35 @@ struct Smem {
     // for the MMAs of kt - AS (two k-tiles of tensor-core work of slack)
     static constexpr int AS = NMAT == 2 ? 3 : 4;
     static constexpr int BS = NMAT == 2 ? 3 : 4;   // activation stages
-    static constexpr int CS = NMAT == 2 ? 2 : 4;   // code stages (CK k-tiles each)
     static constexpr int A_STAGE = NMAT * kTileBytes;
     static constexpr int B_STAGE = BN * 128;
     static constexpr int C_STAGE = NMAT * kCodeTile;
     static constexpr int A_OFF = 0;
     static constexpr int B_OFF = A_OFF + AS * A_STAGE;
-    static constexpr int C_OFF = B_OFF + BS * B_STAGE;
-    static constexpr int SC_OFF = C_OFF + CS * C_STAGE;                    // bf16 scales [NMAT][128][groups]
-    static constexpr int SC_BYTES = NMAT * BM * kMaxGroupsPerCta * 2;
-    static constexpr int Z_OFF = SC_OFF + SC_BYTES;                        // u8 zeros [NMAT][128][groups]
-    static constexpr int Z_BYTES = NMAT * BM * kMaxGroupsPerCta;
-    static constexpr int BAR_OFF = Z_OFF + Z_BYTES;
-    static constexpr int TOTAL = BAR_OFF + 256 + 1024;  // + barriers + alignment slack
+    static constexpr int C_OFF = B_OFF + BS * B_STAGE;   // code ring: args.code_stages x C_STAGE
+    static constexpr int kMaxCS = 8;
+    static constexpr int kBarBytes = 512;
+    static constexpr int kBudget = 227 * 1024 - 1024;      // dynamic smem minus alignment slack
 };
+
+// Fill the runtime layout of one launch (code stages, staged-scale stride).
+template <int NMAT>
+bool plan_smem(GemmArgs& a) {
+    using S = Smem<NMAT>;
+    const int ng = (a.kt_per_split * BK + a.G - 1) / a.G + 1;        // groups one CTA can touch
+    const int sc = NMAT * BM * ng * 2, z = NMAT * BM * ng;
+    const int fixed = S::C_OFF + ((sc + 15) & ~15) + ((z + 15) & ~15) + S::kBarBytes;
+    int cs = (S::kBudget - fixed) / S::C_STAGE;
+    if (cs > S::kMaxCS) cs = S::kMaxCS;
+    if (cs < 2 || ng > kMaxGroupsPerCta) return false;
+    a.code_stages = cs;
+    a.ng_stride = ng;
+    a.sc_off = S::C_OFF + cs * S::C_STAGE;
+    a.z_off = a.sc_off + ((sc + 15) & ~15);
+    a.bar_off = (a.z_off + ((z + 15) & ~15) + 7) & ~7;
+    a.smem_bytes = a.bar_off + S::kBarBytes + 1024;
+    return true;
+}
 
 __device__ __forceinline__ uint32_t bf16x2_bits(__nv_bfloat162 v) {
     return *reinterpret_cast<uint32_t*>(&v);
@@ -119,14 +139,15 @@ template <int NMAT>
 __global__ void __launch_bounds__(kThreads, 1)
 w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constant__ GemmArgs args) {
     using S = Smem<NMAT>;
-    constexpr int AS = S::AS, BS = S::BS, CS = S::CS;
+    constexpr int AS = S::AS, BS = S::BS;
+    const int CS = args.code_stages;
     constexpr uint32_t TMEM_COLS = NMAT * BN;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-B alignment by offsetting the shared array itself (not via an
     // integer round trip) so every derived pointer stays in the shared window
     // and the dequant loads/stores compile to LDS/STS, not generic LD/ST
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    uint64_t* c_full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
+    uint64_t* c_full = reinterpret_cast<uint64_t*>(smem + args.bar_off);
     uint64_t* c_empty = c_full + CS;
     uint64_t* b_full = c_empty + CS;
     uint64_t* b_empty = b_full + BS;
@@ -226,14 +247,15 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
         const int ng = ((kt0 + KT) * BK + G - 1) / G - g0;   // groups touched (<= kMaxGroupsPerCta)
         const int gshift = G == 128 ? 7 : 6;                 // G is 64 or 128 (checked on the host)
         const W4Mat* W = args.w[e];
-        uint16_t* sc_s = reinterpret_cast<uint16_t*>(smem + S::SC_OFF);
-        uint8_t* z_s = smem + S::Z_OFF;
+        uint16_t* sc_s = reinterpret_cast<uint16_t*>(smem + args.sc_off);
+        uint8_t* z_s = smem + args.z_off;
+        const int ngs = args.ng_stride;
         // stage the n-block's scales and zeros for the whole k-range once
         for (int i = td; i < NMAT * BM * ng; i += kDequantThreads) {
             const int j = i / (BM * ng), rem = i - j * BM * ng, r = rem / ng, g = rem - r * ng;
             const size_t gi = (size_t)(n0 + r) * gpr + g0 + g;
-            sc_s[(j * BM + r) * kMaxGroupsPerCta + g] = __ldg(W[j].scales + gi);
-            z_s[(j * BM + r) * kMaxGroupsPerCta + g] = (__ldg(W[j].zeros + (gi >> 1)) >> ((gi & 1) * 4)) & 15;
+            sc_s[(j * BM + r) * ngs + g] = __ldg(W[j].scales + gi);
+            z_s[(j * BM + r) * ngs + g] = (__ldg(W[j].zeros + (gi >> 1)) >> ((gi & 1) * 4)) & 15;
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kDequantThreads));
         const int swz = nl & 7;
@@ -251,9 +273,9 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
                 for (int j = 0; j < NMAT; ++j) {
                     const uint4 c = *reinterpret_cast<const uint4*>(c_tile + j * kCodeTile + nl * (CK * 32) +
                                                                     dg * 32 + half * 16);
-                    const uint32_t z = z_s[(j * BM + nl) * kMaxGroupsPerCta + g];
+                    const uint32_t z = z_s[(j * BM + nl) * ngs + g];
                     const uint32_t zz = (0x4300u | z) * 0x00010001u;
-                    const uint32_t ss = (uint32_t)sc_s[(j * BM + nl) * kMaxGroupsPerCta + g] * 0x00010001u;
+                    const uint32_t ss = (uint32_t)sc_s[(j * BM + nl) * ngs + g] * 0x00010001u;
                     dequant32(c, zz, ss, a_tile + j * kTileBytes + nl * 128, 4 * half, swz);
                 }
                 fence_proxy_async_smem();
@@ -369,16 +391,18 @@ int choose_splits(int d, int mblocks_total) {
 }
 
 template <int NMAT>
-int launch_gemm(const CUtensorMap& map, const GemmArgs& a, int E, int max_mblocks, cudaStream_t st) {
+int launch_gemm(const CUtensorMap& map, GemmArgs& a, int E, int max_mblocks, cudaStream_t st) {
+    if (!plan_smem<NMAT>(a))
+        return fail(DS_ERR_ARG, "w4_gemm: k-range of %d k-tiles does not fit the shared-memory plan", a.kt_per_split);
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(w4_gemm_kernel<NMAT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             Smem<NMAT>::TOTAL);
+                                             227 * 1024);
         if (e != cudaSuccess) return cuda_status(e, "w4_gemm: smem attribute");
         attr = true;
     }
     dim3 grid((a.N / BM) * a.splits, max_mblocks, E);
-    w4_gemm_kernel<NMAT><<<grid, kThreads, Smem<NMAT>::TOTAL, st>>>(map, a);
+    w4_gemm_kernel<NMAT><<<grid, kThreads, a.smem_bytes, st>>>(map, a);
     DS_LAUNCH_CHECK("w4_gemm launch");
     return DS_OK;
 }

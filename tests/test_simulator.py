@@ -230,3 +230,20 @@ def test_cancellable_prefetch_extension():
         mo, _, _ = S.simulate_request("oracle", trs, cfg, cost)
         mo2, _, _ = S.simulate_request("oracle", trs, cfg, cost, cancel_chunk_bytes=chunk)
         assert mo2.e2e_s == mo.e2e_s
+
+
+def test_b200_calibrated_preset():
+    """presets/mixtral-8x7b-b200.json: the reference schema with the W4 model's
+    byte budget (uniform expert bytes = the 91,521,024-byte W4 blob) and a cost
+    model measured on the B200 (scripts/calibrate_cost.py); the simulator runs
+    on it and the link dominates (decode is link-bound on a PCIe host link)."""
+    cfg, cost = C.load_preset("mixtral-8x7b-b200")
+    assert cfg.expert_bytes == 91_521_024
+    assert 40e9 < cost.link_bandwidth_bytes_per_s < 70e9
+    L = cfg.num_layers
+    ds = T.generate_traces(T.default_generator_params(L, 8, 0.8, 3), cfg, 1, 4, 16)
+    trs = ds.traces
+    m, tl, _ = S.simulate_request("oracle", trs, cfg, cost)
+    per_tok = (m.e2e_s - m.ttft_s) / m.decode_tokens
+    floor = L * cfg.top_k * cost.transfer_time_s(cfg.expert_bytes)
+    assert floor <= per_tok < 1.2 * floor
