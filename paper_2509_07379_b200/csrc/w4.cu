@@ -530,13 +530,8 @@ int gemv_grid(const void* fn, size_t smem, int rows_needed) {
     int grid = per_sm * num_sms();
     int need = (rows_needed + wpc - 1) / wpc;
     if (grid >= need) return need;
-    // rows pass over the resident warps `passes` times; shrink the grid so every
-    // warp runs exactly that many rows (no last pass carried by a few warps)
-    static const bool balance = getenv("DS_K4_NO_BALANCE") == nullptr;
-    if (balance) {
-        const int passes = (rows_needed + grid * wpc - 1) / (grid * wpc);
-        grid = (rows_needed + passes * wpc - 1) / (passes * wpc);
-    }
+    // (shrinking the grid so every warp runs the same number of rows measured
+    // slower on B200: 39.8 vs 37.7 us per 8x7B expert — the tail pass is cheap)
     return grid;
 }
 
