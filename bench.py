@@ -53,6 +53,8 @@ def parse():
                     help="paper-faithful decode: whole-expert prefetch, no cancellation of wrong prefetches")
     ap.add_argument("--chunk-mb", type=float, default=8.0)
     ap.add_argument("--link-depth", type=int, default=2)
+    ap.add_argument("--spec-chunk-mb", type=float, default=0.5,
+                    help="chunk size of speculative (predicted) prefetches until the gate confirms them")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--ep", action="store_true",
                     help="under torchrun: expert parallelism (rank r owns experts e %% N == r, per-rank pinned "
@@ -270,7 +272,7 @@ def run_ours(args):
     eng = Engine(shape, args.policy if args.policy != "oracle" else "duoserve", seed=args.seed, device=dev,
                  predictor=net, pop=pop, aff=aff, max_seq=args.prefill + args.decode + 8,
                  max_prefill=args.prefill, cancel_mispredicted=not args.no_cancel, chunk_mb=args.chunk_mb,
-                 link_depth=args.link_depth, ep=ep)
+                 link_depth=args.link_depth, ep=ep, spec_chunk_mb=args.spec_chunk_mb)
     # replicas: an independent request per rank; EP: every rank serves the same request
     gen = torch.Generator().manual_seed(args.seed + (0 if ep else 1000 * rank))
     ids_host = torch.randint(0, shape.vocab, (args.prefill,), generator=gen).pin_memory()

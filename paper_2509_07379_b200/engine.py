@@ -155,7 +155,8 @@ class LinkQueue:
     With cancel=False and one chunk per expert it is exactly the paper's
     schedule (whole-expert prefetch, then blocking re-fetch)."""
 
-    def __init__(self, cache: "ExpertCache", chunk_bytes: int, depth: int, cancel: bool):
+    def __init__(self, cache: "ExpertCache", chunk_bytes: int, depth: int, cancel: bool,
+                 spec_chunk_bytes: int = 2 << 20):
         import ctypes as C
         from . import _lib
         self.C, self.lib = C, _lib
@@ -164,7 +165,7 @@ class LinkQueue:
         self.chunk = blob if chunk_bytes <= 0 else min(chunk_bytes, blob)
         self.depth = depth
         self.cancel_enabled = cancel
-        self.spec_chunk = min(self.chunk, 2 << 20)
+        self.spec_chunk = min(self.chunk, spec_chunk_bytes)
         h = C.c_void_p()
         _lib.call("ds_link_create", C.c_void_p(cache.copy_stream.cuda_stream), self.chunk, depth, C.byref(h))
         self.handle = h
@@ -315,7 +316,7 @@ class Engine:
                  predictor: ExpertMLP | None = None, pop=None, aff=None, oracle_paths=None,
                  max_seq: int = 2048, max_prefill: int = 2048, cancel_mispredicted: bool = True,
                  chunk_mb: float = 4.0, link_depth: int = 2, use_graphs: bool = True,
-                 ep: EPConfig | None = None, collect_stats: bool = False):
+                 ep: EPConfig | None = None, collect_stats: bool = False, spec_chunk_mb: float = 0.5):
         self.shape = shape
         self.policy = SchedulerPolicy(policy)
         self.device = torch.device(device)
@@ -334,7 +335,8 @@ class Engine:
         self.cache = ExpertCache(self.store, self.n_slots, self.device)
         self.cancel_mispredicted = cancel_mispredicted
         self.link = LinkQueue(self.cache, int(chunk_mb * 2**20) if cancel_mispredicted else 0,
-                              link_depth if cancel_mispredicted else 2, cancel_mispredicted)
+                              link_depth if cancel_mispredicted else 2, cancel_mispredicted,
+                              spec_chunk_bytes=int(spec_chunk_mb * 2**20))
         self.kv = KVCache(sh, max_seq, self.device)
         self.cos, self.sin = rope_tables(sh, max_seq, self.device)
         self.driver = None
@@ -774,7 +776,7 @@ class Engine:
         exact = sum(r["pred"] == r["gate"] for r in dec)
         n = len(dec)
         return {"policy": self.policy.value, "cancel_mispredicted": self.cancel_mispredicted,
-                "chunk_bytes": self.link.chunk, **self.link.stats(),
+                "chunk_bytes": self.link.chunk, "spec_chunk_bytes": self.link.spec_chunk, **self.link.stats(),
                 "prefetch_hits": hits, "prefetch_misses": miss,
                 "topk_hit_rate": round(exact / n, 4) if n else None,
                 "at_least_one_rate": round(sum(bool(set(r["pred"]) & set(r["gate"])) for r in dec) / n, 4)
