@@ -171,6 +171,14 @@ int ds_w4_swiglu_gemv(const void *x, int R, const ds_w4_expert *e, int d, int ff
                       void *stream);
 int ds_w4_down_gemv(const void *h, int R, const ds_w4_expert *e, int d, int ff, int G,
                     const float *route_w, int route_stride, float *acc, void *stream);
+/* One expert's decode FFN in one call: ds_w4_swiglu_gemv then
+ * ds_w4_down_gemv (the down GEMV launched as a programmatic dependent of the
+ * SwiGLU GEMV).  ev_start / ev_end (cudaEvent_t, may be NULL) are recorded on
+ * `stream` immediately around the two launches: the kernel-time span a
+ * profiler reads without host latency in it.                              */
+int ds_w4_expert_gemv(const void *x, int R, const ds_w4_expert *e, int d, int ff, int G, void *h,
+                      const float *route_w, int route_stride, float *acc, void *ev_start, void *ev_end,
+                      void *stream);
 /* out[r] = bf16(resid[r] + acc[r]) and acc zeroed for the next layer.      */
 int ds_combine_finalize(float *acc, const void *resid, int R, int d, void *out, void *stream);
 /* Prefill grouped FFN (K3): for experts e in [0,E) (E <= 16): rows
@@ -186,6 +194,12 @@ size_t ds_w4_grouped_ffn_workspace(int total_rows, int d, int ff);
 int ds_w4_grouped_ffn(const void *xperm, const int32_t *offsets, int E, const ds_w4_expert *experts,
                       int d, int ff, int G, void *h, float *y, void *workspace,
                       size_t workspace_bytes, void *stream);
+/* Same, with cudaEvent_t ev_start / ev_end (may be NULL) recorded on `stream`
+ * right before the first and after the last launch (host-side tensor-map
+ * preparation excluded): the kernel-time span a profiler reads.           */
+int ds_w4_grouped_ffn_ev(const void *xperm, const int32_t *offsets, int E, const ds_w4_expert *experts,
+                         int d, int ff, int G, void *h, float *y, void *workspace,
+                         size_t workspace_bytes, void *ev_start, void *ev_end, void *stream);
 
 /* ========================================================================
  * K6 — host->device expert link (copy engine), native scheduler thread.

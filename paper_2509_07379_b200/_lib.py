@@ -79,6 +79,7 @@ _SIGS = {
     "ds_w4_dequant": (_I, [C.POINTER(W4Linear), _I, _I, _I, _P, _P]),
     "ds_w4_swiglu_gemv": (_I, [_P, _I, C.POINTER(W4Expert), _I, _I, _I, _P, _P]),
     "ds_w4_down_gemv": (_I, [_P, _I, C.POINTER(W4Expert), _I, _I, _I, _P, _I, _P, _P]),
+    "ds_w4_expert_gemv": (_I, [_P, _I, C.POINTER(W4Expert), _I, _I, _I, _P, _P, _I, _P, _P, _P, _P]),
     "ds_combine_finalize": (_I, [_P, _P, _I, _I, _P, _P]),
     "ds_w4_grouped_ffn_workspace": (_SZ, [_I, _I, _I]),
     "ds_link_create": (_I, [_P, _SZ, _I, C.POINTER(_P)]),
@@ -94,6 +95,8 @@ _SIGS = {
     "ds_link_trace": (_I, [_P, _I]),
     "ds_link_trace_read": (_I, [_P, _P, C.POINTER(C.c_float), C.POINTER(C.c_float), _SZ, C.POINTER(_SZ)]),
     "ds_w4_grouped_ffn": (_I, [_P, C.POINTER(_I), _I, C.POINTER(W4Expert), _I, _I, _I, _P, _P, _P, _SZ, _P]),
+    "ds_w4_grouped_ffn_ev": (_I, [_P, C.POINTER(_I), _I, C.POINTER(W4Expert), _I, _I, _I, _P, _P, _P, _SZ, _P, _P,
+                                  _P]),
 }
 
 _lib = None

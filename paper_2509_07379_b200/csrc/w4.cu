@@ -758,6 +758,25 @@ extern "C" int ds_w4_down_gemv(const void* h, int R, const ds_w4_expert* e, int 
     return DS_OK;
 }
 
+extern "C" int ds_w4_expert_gemv(const void* x, int R, const ds_w4_expert* e, int d, int ff, int G, void* h,
+                                 const float* route_w, int route_stride, float* acc, void* ev_start, void* ev_end,
+                                 void* stream) {
+    cudaStream_t st = as_stream(stream);
+    if (ev_start) {
+        cudaError_t er = cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_start), st);
+        if (er != cudaSuccess) return cuda_status(er, "ds_w4_expert_gemv: event");
+    }
+    int rc = ds_w4_swiglu_gemv(x, R, e, d, ff, G, h, stream);
+    if (rc) return rc;
+    rc = ds_w4_down_gemv(h, R, e, d, ff, G, route_w, route_stride, acc, stream);
+    if (rc) return rc;
+    if (ev_end) {
+        cudaError_t er = cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_end), st);
+        if (er != cudaSuccess) return cuda_status(er, "ds_w4_expert_gemv: event");
+    }
+    return DS_OK;
+}
+
 extern "C" int ds_combine_finalize(float* acc, const void* resid, int R, int d, void* out,
                                    void* stream) {
     DS_CHECK_ARG(R >= 0 && d > 0, "ds_combine_finalize: bad shape");

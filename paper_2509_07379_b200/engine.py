@@ -611,12 +611,12 @@ class Engine:
     def _prefill_ffn(self, e: int, slot: int, off) -> None:
         lo, hi = off[e], off[e + 1]
         st = self.cache.acquire(slot)
-        ev = self.prof.start() if self.prof else None
+        evs = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) if self.prof else (None, None)
         ops.grouped_ffn(self.p_xperm[lo:hi], [0, hi - lo], [st], self.d, self.ff, self.G,
-                        self.p_h[lo:hi], self.p_y[lo:hi], self.p_ws)
+                        self.p_h[lo:hi], self.p_y[lo:hi], self.p_ws, *evs)
         if self.prof:
-            self.prof.stop("K3 w4_grouped_ffn (tcgen05)", ev, self.store.blob_bytes,
-                           6.0 * (hi - lo) * self.d * self.ff)
+            self.prof.add("K3 w4_grouped_ffn (tcgen05)", evs[0], evs[1], self.store.blob_bytes,
+                          6.0 * (hi - lo) * self.d * self.ff)
 
     def _prefill_combine(self, h, T, w, idx):
         out = torch.empty_like(h)
@@ -716,11 +716,12 @@ class Engine:
 
     def _decode_ffn(self, a, st, j: int) -> None:
         """K4: acc += w_j * W2 (silu(a W1) * (a W3)) for the expert in slot struct st."""
-        ev = self.prof.start() if self.prof else None
-        ops.swiglu_gemv(a, st, self.d, self.ff, self.G, self.h_buf)
-        ops.down_gemv(self.h_buf, st, self.d, self.ff, self.G, self.w1[0, j:], 1, self.acc)
         if self.prof:
-            self.prof.stop("K4 w4_swiglu_gemv+down_gemv", ev, self.store.blob_bytes)
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ops.expert_gemv(a, st, self.d, self.ff, self.G, self.h_buf, self.w1[0, j:], 1, self.acc, ev0, ev1)
+            self.prof.add("K4 w4_swiglu_gemv+down_gemv", ev0, ev1, self.store.blob_bytes)
+        else:
+            ops.expert_gemv(a, st, self.d, self.ff, self.G, self.h_buf, self.w1[0, j:], 1, self.acc)
 
     def _decode_combine(self, h, out):
         if out is None:
@@ -863,6 +864,10 @@ class KernelProfiler:
         ev = torch.cuda.Event(enable_timing=True)
         ev.record()
         return ev
+
+    def add(self, name: str, ev0, ev1, nbytes: float, flops: float = 0.0):
+        """A span whose events were recorded elsewhere (natively, around the launches)."""
+        self.spans.setdefault(name, []).append((ev0, ev1, nbytes, flops))
 
     def stop(self, name: str, ev0, nbytes: float, flops: float = 0.0):
         ev1 = torch.cuda.Event(enable_timing=True)

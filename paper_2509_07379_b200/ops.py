@@ -99,6 +99,18 @@ def down_gemv(h: torch.Tensor, e: _lib.W4Expert, d: int, ff: int, G: int, route_
     _count("ds_w4_down_gemv", _gemv_passes(h.shape[0], G))
 
 
+def expert_gemv(x: torch.Tensor, e: _lib.W4Expert, d: int, ff: int, G: int, h: torch.Tensor, route_w: torch.Tensor,
+                route_stride: int, acc: torch.Tensor, ev_start=None, ev_end=None) -> None:
+    """K4 for one expert in one C call (SwiGLU GEMV + PDL down GEMV); the
+    optional torch.cuda.Events are recorded natively around the launches."""
+    evs = [C.c_void_p(ev.cuda_event) if ev is not None else None for ev in (ev_start, ev_end)]
+    _lib.call("ds_w4_expert_gemv", ptr(x), x.shape[0], C.byref(e), d, ff, G, ptr(h), ptr(route_w), route_stride,
+              ptr(acc), evs[0], evs[1], stream_ptr())
+    n = _gemv_passes(x.shape[0], G)
+    _count("ds_w4_swiglu_gemv", n)
+    _count("ds_w4_down_gemv", n)
+
+
 def combine_finalize(acc: torch.Tensor, resid: torch.Tensor, out: torch.Tensor) -> None:
     _lib.call("ds_combine_finalize", ptr(acc), ptr(resid), resid.shape[0], resid.shape[1], ptr(out), stream_ptr())
     _count("ds_combine_finalize")
@@ -109,12 +121,19 @@ def grouped_ffn_workspace(rows: int, d: int, ff: int) -> int:
 
 
 def grouped_ffn(xperm: torch.Tensor, offsets: list, experts: list, d: int, ff: int, G: int, h: torch.Tensor,
-                y: torch.Tensor, ws: torch.Tensor) -> None:
+                y: torch.Tensor, ws: torch.Tensor, ev_start=None, ev_end=None) -> None:
+    """K3.  ev_start / ev_end (torch.cuda.Event, optional) are recorded natively
+    around the launches (host-side preparation excluded)."""
     E = len(experts)
     off = (C.c_int * (E + 1))(*[int(o) for o in offsets])
     arr = (_lib.W4Expert * E)(*experts)
-    _lib.call("ds_w4_grouped_ffn", ptr(xperm), off, E, arr, d, ff, G, ptr(h), ptr(y), ptr(ws), ws.numel(),
-              stream_ptr())
+    if ev_start is None and ev_end is None:
+        _lib.call("ds_w4_grouped_ffn", ptr(xperm), off, E, arr, d, ff, G, ptr(h), ptr(y), ptr(ws), ws.numel(),
+                  stream_ptr())
+    else:
+        evs = [C.c_void_p(ev.cuda_event) if ev is not None else None for ev in (ev_start, ev_end)]
+        _lib.call("ds_w4_grouped_ffn_ev", ptr(xperm), off, E, arr, d, ff, G, ptr(h), ptr(y), ptr(ws), ws.numel(),
+                  evs[0], evs[1], stream_ptr())
     _count("ds_w4_grouped_ffn", 3)
 
 

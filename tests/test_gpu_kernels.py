@@ -197,3 +197,40 @@ def test_w4_grouped_ffn_tcgen05(d, ff, rows, cuda):
         y_ref = hb @ W2.T
         rel2 = ((y[lo:hi].double() - y_ref).norm() / y_ref.norm()).item()
         assert rel2 < 5e-5, (i, rel2)           # f32 accumulation over K up to 16384
+
+
+def test_expert_gemv_and_timed_grouped_ffn_match_split_calls(cuda):
+    """ds_w4_expert_gemv (SwiGLU + PDL down in one call, native timing events)
+    equals the two separate calls bit for bit; ds_w4_grouped_ffn_ev equals
+    ds_w4_grouped_ffn and records a positive span."""
+    import torch
+    from paper_2509_07379_b200 import ops
+    d, ff, G = 4096, 14336, 128
+    offs, total = _layout(d, ff, G)
+    blob = torch.zeros(total, dtype=torch.uint8, device=cuda)
+    _lib.call("ds_w4_generate", 11, 0, 2, d, ff, G, _lib.ptr(blob), _lib.stream_ptr())
+    e = _expert_struct(blob, offs)
+    x = _rand_bf16((1, d), 1.0, torch.Generator().manual_seed(3)).to(cuda)
+    rw = torch.tensor([0.75], device=cuda)
+    h1 = torch.empty((1, ff), dtype=torch.bfloat16, device=cuda)
+    a1 = torch.zeros((1, d), device=cuda)
+    ops.swiglu_gemv(x, e, d, ff, G, h1)
+    ops.down_gemv(h1, e, d, ff, G, rw, 1, a1)
+    h2 = torch.empty_like(h1)
+    a2 = torch.zeros_like(a1)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ops.expert_gemv(x, e, d, ff, G, h2, rw, 1, a2, ev0, ev1)
+    torch.cuda.synchronize()
+    assert torch.equal(h1, h2) and torch.equal(a1, a2)
+    assert ev0.elapsed_time(ev1) > 0
+    R = 128
+    xp = _rand_bf16((R, d), 1.0, torch.Generator().manual_seed(4)).to(cuda)
+    ws = torch.empty(max(ops.grouped_ffn_workspace(R, d, ff), 16), dtype=torch.uint8, device=cuda)
+    hh1, y1 = torch.empty((R, ff), dtype=torch.bfloat16, device=cuda), torch.empty((R, d), device=cuda)
+    hh2, y2 = torch.empty_like(hh1), torch.empty_like(y1)
+    ops.grouped_ffn(xp, [0, R], [e], d, ff, G, hh1, y1, ws)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ops.grouped_ffn(xp, [0, R], [e], d, ff, G, hh2, y2, ws, e0, e1)
+    torch.cuda.synchronize()
+    assert torch.equal(hh1, hh2) and torch.equal(y1, y2)
+    assert e0.elapsed_time(e1) > 0
