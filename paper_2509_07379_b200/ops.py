@@ -99,11 +99,26 @@ def down_gemv(h: torch.Tensor, e: _lib.W4Expert, d: int, ff: int, G: int, route_
     _count("ds_w4_down_gemv", _gemv_passes(h.shape[0], G))
 
 
+def _native_events(*evs):
+    """cudaEvent_t handles of torch events for the C side to (re-)record.
+    torch creates the CUDA event lazily on its first record, so record each
+    once here (a placeholder the native record overwrites; it also marks the
+    torch wrapper as recorded for elapsed_time)."""
+    out = []
+    for ev in evs:
+        if ev is None:
+            out.append(None)
+            continue
+        ev.record()
+        out.append(C.c_void_p(ev.cuda_event))
+    return out
+
+
 def expert_gemv(x: torch.Tensor, e: _lib.W4Expert, d: int, ff: int, G: int, h: torch.Tensor, route_w: torch.Tensor,
                 route_stride: int, acc: torch.Tensor, ev_start=None, ev_end=None) -> None:
     """K4 for one expert in one C call (SwiGLU GEMV + PDL down GEMV); the
     optional torch.cuda.Events are recorded natively around the launches."""
-    evs = [C.c_void_p(ev.cuda_event) if ev is not None else None for ev in (ev_start, ev_end)]
+    evs = _native_events(ev_start, ev_end)
     _lib.call("ds_w4_expert_gemv", ptr(x), x.shape[0], C.byref(e), d, ff, G, ptr(h), ptr(route_w), route_stride,
               ptr(acc), evs[0], evs[1], stream_ptr())
     n = _gemv_passes(x.shape[0], G)
@@ -131,7 +146,7 @@ def grouped_ffn(xperm: torch.Tensor, offsets: list, experts: list, d: int, ff: i
         _lib.call("ds_w4_grouped_ffn", ptr(xperm), off, E, arr, d, ff, G, ptr(h), ptr(y), ptr(ws), ws.numel(),
                   stream_ptr())
     else:
-        evs = [C.c_void_p(ev.cuda_event) if ev is not None else None for ev in (ev_start, ev_end)]
+        evs = _native_events(ev_start, ev_end)
         _lib.call("ds_w4_grouped_ffn_ev", ptr(xperm), off, E, arr, d, ff, G, ptr(h), ptr(y), ptr(ws), ws.numel(),
                   evs[0], evs[1], stream_ptr())
     _count("ds_w4_grouped_ffn", 3)
