@@ -6,7 +6,7 @@
 //   GEMM2  Y[m, n'] = (H W2)[m, n']  (f32, split-K partials reduced in a
 //                                      fixed order -> deterministic)
 // Swap-AB: the weight output dimension is the UMMA M side (128 rows per
-// CTA tile), the expert's token rows are the UMMA N side (BN = 128), so
+// CTA tile), the expert's token rows are the UMMA N side (TN = 128, or 256 once an expert has more than 128 rows), so
 // small per-expert row counts still fill M=128 tiles.
 //
 // Per CTA (one 128 x BN output tile, one expert):
@@ -27,6 +27,8 @@
 #include "sm100.cuh"
 
 #include <cuda.h>
+
+#include <algorithm>
 
 namespace ds {
 namespace {
@@ -74,14 +76,14 @@ constexpr int kMaxGroupsPerCta = 64;            // staged scales/zeros per row (
 // Three decoupled rings: packed codes (TMA from HBM, deepest), activation
 // tiles (TMA, L2-resident) and dequantised bf16 weight tiles (written by the
 // dequant warps, read by the tensor cores).
-template <int NMAT>
+template <int NMAT, int TN>
 struct Smem {
     // dequantised weight stages: >= 3 so the dequant of k-tile kt only waits
     // for the MMAs of kt - AS (two k-tiles of tensor-core work of slack)
-    static constexpr int AS = NMAT == 2 ? 3 : 4;
-    static constexpr int BS = NMAT == 2 ? 3 : 4;   // activation stages
+    static constexpr int AS = (NMAT == 2 && TN == 256) ? 2 : (NMAT == 2 ? 3 : 4);
+    static constexpr int BS = TN == 256 ? (NMAT == 2 ? 2 : 3) : (NMAT == 2 ? 3 : 4);   // activation stages
     static constexpr int A_STAGE = NMAT * kTileBytes;
-    static constexpr int B_STAGE = BN * 128;
+    static constexpr int B_STAGE = TN * 128;
     static constexpr int C_STAGE = NMAT * kCodeTile;
     static constexpr int A_OFF = 0;
     static constexpr int B_OFF = A_OFF + AS * A_STAGE;
@@ -92,9 +94,9 @@ struct Smem {
 };
 
 // Fill the runtime layout of one launch (code stages, staged-scale stride).
-template <int NMAT>
+template <int NMAT, int TN>
 bool plan_smem(GemmArgs& a) {
-    using S = Smem<NMAT>;
+    using S = Smem<NMAT, TN>;
     const int ng = (a.kt_per_split * BK + a.G - 1) / a.G + 1;        // groups one CTA can touch
     const int sc = NMAT * BM * ng * 2, z = NMAT * BM * ng;
     const int fixed = S::C_OFF + ((sc + 15) & ~15) + ((z + 15) & ~15) + S::kBarBytes;
@@ -135,13 +137,13 @@ __device__ __forceinline__ void dequant32(const uint4 c, uint32_t zz, uint32_t s
     }
 }
 
-template <int NMAT>
+template <int NMAT, int TN>
 __global__ void __launch_bounds__(kThreads, 1)
 w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constant__ GemmArgs args) {
-    using S = Smem<NMAT>;
+    using S = Smem<NMAT, TN>;
     constexpr int AS = S::AS, BS = S::BS;
     const int CS = args.code_stages;
-    constexpr uint32_t TMEM_COLS = NMAT * BN;
+    constexpr uint32_t TMEM_COLS = NMAT * TN;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-B alignment by offsetting the shared array itself (not via an
     // integer round trip) so every derived pointer stays in the shared window
@@ -158,7 +160,7 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
 
     const int e = blockIdx.z;
     const int rows = args.rows[e];
-    const int m0 = blockIdx.y * BN;
+    const int m0 = blockIdx.y * TN;
     if (m0 >= rows) return;                       // whole CTA exits before any barrier
     const int n_blocks = args.N / BM;
     const int nb = blockIdx.x % n_blocks;
@@ -212,7 +214,7 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
     } else if (warp == 2) {
         // -------------------------------------------------------- MMA issuer
         if (lane == 0) {
-            const uint32_t idesc = idesc_bf16_f32(BM, BN);
+            const uint32_t idesc = idesc_bf16_f32(BM, TN);
             for (int kt = 0; kt < KT; ++kt) {
                 const int sa = kt % AS, sb = kt % BS;
                 mbar_wait(&b_full[sb], (kt / BS) & 1);
@@ -226,7 +228,7 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
                     for (int j = 0; j < NMAT; ++j) {
                         const uint64_t adesc = umma_desc_sw128(a_addr + j * kTileBytes);
                         // advance along K inside the swizzle atom: +32 B = +2 (16-B units)
-                        mma_bf16(tmem_base + j * BN, adesc + 2 * kk, bdesc + 2 * kk, idesc,
+                        mma_bf16(tmem_base + j * TN, adesc + 2 * kk, bdesc + 2 * kk, idesc,
                                  (kt | kk) != 0);
                     }
                 }
@@ -292,13 +294,13 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
             tc_fence_after();
             const uint32_t lane_addr = tmem_base + ((uint32_t)(32 * q) << 16);
             const int row0 = args.row_start[e] + m0;
-            const int valid = min(BN, rows - m0);
-            for (int c0 = 0; c0 < BN; c0 += 16) {
+            const int valid = min(TN, rows - m0);
+            for (int c0 = 0; c0 < TN; c0 += 16) {
                 uint32_t d1[16];
                 tmem_ld16(lane_addr + c0, d1);
                 if constexpr (NMAT == 2) {
                     uint32_t d3[16];
-                    tmem_ld16(lane_addr + BN + c0, d3);
+                    tmem_ld16(lane_addr + TN + c0, d3);
                     tmem_ld_wait();
                     __nv_bfloat16* H = static_cast<__nv_bfloat16*>(args.out);
 #pragma unroll
@@ -369,12 +371,12 @@ int make_codes_map(CUtensorMap* map, const void* codes, int N, int K) {
     return DS_OK;
 }
 
-int make_act_map(CUtensorMap* map, const void* base, int rows, int K) {
+int make_act_map(CUtensorMap* map, const void* base, int rows, int K, int tn) {
     EncodeTiledFn fn = encode_fn();
     if (!fn) return fail(DS_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
     cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)K * 2};
-    cuuint32_t box[2] = {BK, BN};
+    cuuint32_t box[2] = {BK, (cuuint32_t)tn};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
                     estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -390,19 +392,19 @@ int choose_splits(int d, int mblocks_total) {
     return s;
 }
 
-template <int NMAT>
+template <int NMAT, int TN>
 int launch_gemm(const CUtensorMap& map, GemmArgs& a, int E, int max_mblocks, cudaStream_t st) {
-    if (!plan_smem<NMAT>(a))
+    if (!plan_smem<NMAT, TN>(a))
         return fail(DS_ERR_ARG, "w4_gemm: k-range of %d k-tiles does not fit the shared-memory plan", a.kt_per_split);
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(w4_gemm_kernel<NMAT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(w4_gemm_kernel<NMAT, TN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              227 * 1024);
         if (e != cudaSuccess) return cuda_status(e, "w4_gemm: smem attribute");
         attr = true;
     }
     dim3 grid((a.N / BM) * a.splits, max_mblocks, E);
-    w4_gemm_kernel<NMAT><<<grid, kThreads, a.smem_bytes, st>>>(map, a);
+    w4_gemm_kernel<NMAT, TN><<<grid, kThreads, a.smem_bytes, st>>>(map, a);
     DS_LAUNCH_CHECK("w4_gemm launch");
     return DS_OK;
 }
@@ -420,9 +422,13 @@ int splits_for(int d, int ff, int G, int mblocks) {
 using namespace ds;
 
 extern "C" size_t ds_w4_grouped_ffn_workspace(int total_rows, int d, int ff) {
-    const int mb = (total_rows + BN - 1) / BN;
-    const int s = ds::splits_for(d, ff, 64, mb) > ds::splits_for(d, ff, 128, mb) ? ds::splits_for(d, ff, 64, mb)
-                                                                               : ds::splits_for(d, ff, 128, mb);
+    // worst case over the token tile (128 or 256 rows) and G: fewer m-blocks can mean more K splits
+    int s = 1;
+    for (int tn : {128, 256})
+        for (int g : {64, 128}) {
+            const int v = ds::splits_for(d, ff, g, (total_rows + tn - 1) / tn);
+            s = v > s ? v : s;
+        }
     return (size_t)s * total_rows * d * sizeof(float);
 }
 
@@ -458,13 +464,18 @@ static int grouped_ffn_impl(const void* xperm, const int32_t* offsets, int E, co
     DS_CHECK_ARG(xperm && offsets && experts && h && y, "ds_w4_grouped_ffn: NULL pointer");
     const int total_rows = offsets[E];
     GemmArgs a1{}, a2{};
+    // token tile: 256 rows (UMMA N = 256) once an expert has more than 128 rows,
+    // so its weights are dequantised once instead of once per 128-row block
+    int max_rows = 0;
+    for (int i = 0; i < E; ++i) max_rows = std::max(max_rows, offsets[i + 1] - offsets[i]);
+    const int TN = max_rows > 128 ? 256 : 128;
     int max_mb = 0, mb_total = 0;
     for (int i = 0; i < E; ++i) {
         const int r = offsets[i + 1] - offsets[i];
         DS_CHECK_ARG(r >= 0 && offsets[i] >= 0, "ds_w4_grouped_ffn: offsets must be non-decreasing");
         a1.row_start[i] = a2.row_start[i] = offsets[i];
         a1.rows[i] = a2.rows[i] = r;
-        const int mb = (r + BN - 1) / BN;
+        const int mb = (r + TN - 1) / TN;
         max_mb = mb > max_mb ? mb : max_mb;
         mb_total += mb;
         const ds_w4_linear* L[3] = {&experts[i].w1, &experts[i].w3, &experts[i].w2};
@@ -484,7 +495,7 @@ static int grouped_ffn_impl(const void* xperm, const int32_t* offsets, int E, co
     cudaStream_t st = as_stream(stream);
     // GEMM1: K = d, N = ff
     CUtensorMap map1, map2;
-    int rc = make_act_map(&map1, xperm, total_rows, d);
+    int rc = make_act_map(&map1, xperm, total_rows, d, TN);
     if (rc) return rc;
     a1.K = d; a1.N = ff; a1.G = G; a1.kt_per_split = d / BK; a1.splits = 1;
     a1.total_rows = total_rows; a1.out = h;
@@ -494,10 +505,10 @@ static int grouped_ffn_impl(const void* xperm, const int32_t* offsets, int E, co
         cudaError_t er = cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_start), st);
         if (er != cudaSuccess) return cuda_status(er, "ds_w4_grouped_ffn: event");
     }
-    rc = launch_gemm<2>(map1, a1, E, max_mb, st);
+    rc = TN == 256 ? launch_gemm<2, 256>(map1, a1, E, max_mb, st) : launch_gemm<2, 128>(map1, a1, E, max_mb, st);
     if (rc) return rc;
     // GEMM2: K = ff, N = d, split-K with a deterministic reduction
-    rc = make_act_map(&map2, h, total_rows, ff);
+    rc = make_act_map(&map2, h, total_rows, ff, TN);
     if (rc) return rc;
     const int splits = splits_for(d, ff, G, mb_total);
     const size_t need = (size_t)splits * total_rows * d * sizeof(float);
@@ -510,7 +521,7 @@ static int grouped_ffn_impl(const void* xperm, const int32_t* offsets, int E, co
             return fail(DS_ERR_WORKSPACE, "ds_w4_grouped_ffn: workspace %zu < %zu", workspace_bytes, need);
         a2.out = workspace;
     }
-    rc = launch_gemm<1>(map2, a2, E, max_mb, st);
+    rc = TN == 256 ? launch_gemm<1, 256>(map2, a2, E, max_mb, st) : launch_gemm<1, 128>(map2, a2, E, max_mb, st);
     if (rc) return rc;
     if (splits > 1) {
         const size_t n = (size_t)total_rows * d;

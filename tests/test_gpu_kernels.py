@@ -163,9 +163,11 @@ def _dense(e, d, ff, G, cuda):
 
 
 @pytest.mark.parametrize("d,ff,rows", [(256, 896, [7, 64, 0, 130]), (4096, 14336, [128, 100, 3]),
-                                       (6144, 16384, [200]), (256, 896, [1])])
+                                       (6144, 16384, [200]), (256, 896, [1]), (4096, 14336, [300, 17])])
 def test_w4_grouped_ffn_tcgen05(d, ff, rows, cuda):
-    """K3 (tcgen05/TMEM/TMA) vs an f64 reference on the bit-exact dequantised weights."""
+    """K3 (tcgen05/TMEM/TMA) vs an f64 reference on the bit-exact dequantised weights.
+    Row counts cover the 128-row token tile, the 256-row tile (> 128 rows) and
+    two 256-row m-blocks (300)."""
     G = 128
     offs, total = _layout(d, ff, G)
     E = len(rows)
