@@ -554,8 +554,14 @@ class Engine:
             return
         slot = self._next_ring_slot()
         first = self.owned[0]                    # lowest (owned) expert; 0 on a single GPU
-        self.cache.load(slot, layer, first)
-        self._spec = (slot, layer, first)
+        if self.link.cancel_enabled:
+            # through the native link in small chunks: if the gate leaves `first`
+            # out of A_l its remaining chunks are dropped (the log is unchanged)
+            self.cache.content[slot] = (layer, first)
+            self._spec = (slot, layer, first, self.link.submit(slot, layer, first, speculative=True))
+        else:
+            self.cache.load(slot, layer, first)
+            self._spec = (slot, layer, first, None)
 
     def _moe_prefill(self, l: int, h: torch.Tensor, T: int):
         sh = self.shape
@@ -587,6 +593,13 @@ class Engine:
             spec = self._spec if (self._spec is not None and self._spec[1] == l) else None
             if spec is not None:
                 plan.append((spec[2], spec[0], True))
+                tr = spec[3]
+                if tr is not None:
+                    if spec[2] in A:
+                        self.link.promote(tr)          # confirmed: finish with large chunks
+                        self.link.flush(tr)            # all chunks issued before later copies queue
+                    else:
+                        self.link.cancel(tr)           # wrong guess: drop its remaining chunks
             plan += [(e, self._next_ring_slot(), False) for e in A if not (spec and e == spec[2])]
         self.log.append({"phase": "prefill", "layer": l, "fetch": [e for e, _, _ in plan], "activated": A_all})
         # sliding window over the slot ring: the copy into a slot is queued only

@@ -62,6 +62,23 @@ if "k4" in only:
     t12 = timeit(lambda i: (ops.swiglu_gemv(x, es[i % NB], d, ff, G, h),
                             ops.down_gemv(h, es[i % NB], d, ff, G, rw, 1, acc)), a.iters)
     res["k4_expert"] = {"us": t12 * 1e6, "GBs": total / t12 / 1e9, "frac": total / t12 / 1e9 / peaks["hbm_gbs"]}
+    # the serving loop runs K4 after the GPU idled ~1-2 ms waiting on the host link:
+    # same unit timed after an idle gap (no L2 flush kernel right before it)
+    tis = []
+    for i in range(a.iters + 3):
+        torch.cuda.synchronize()
+        time.sleep(0.002)                       # GPU idle, as while the link streams an expert
+        s_ = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s_)
+        ops.swiglu_gemv(x, es[i % NB], d, ff, G, h)
+        ops.down_gemv(h, es[i % NB], d, ff, G, rw, 1, acc)
+        e1.record(s_)
+        e1.synchronize()
+        if i >= 3:
+            tis.append(e0.elapsed_time(e1) / 1e3)
+    ti = float(np.median(tis))
+    res["k4_expert_after_idle"] = {"us": ti * 1e6, "GBs": total / ti / 1e9, "frac": total / ti / 1e9 / peaks["hbm_gbs"]}
 if "k3" in only:
     R = a.rows
     xp = (torch.randn(R, d, device=dev)).to(torch.bfloat16)
