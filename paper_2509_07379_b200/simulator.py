@@ -316,6 +316,18 @@ def schedule_prefill_layer(st: _State, l: int, activated: dict) -> dict:
         # the rest of A_l streams ascending, one fetch each (fetch-once)
         fetch = [0] + [e for e in A if e != 0]
         for i, e in enumerate(fetch):
+            if i == 0 and e not in activated and st.cancel_ns is not None:
+                # B200 extension: the speculative first transfer is dropped one
+                # chunk after the gate proves it unneeded (log unchanged)
+                slot, free = st.cache.acquire()
+                start = max(st.t_link, t0, free)
+                end = max(start, min(start + st.T, g + st.cancel_ns))
+                st.tl.add("comm", "cancelled", start, end, expert=e, layer=l, phase="prefill")
+                st.cache.load(slot, (l, e), start, end)
+                st.t_link = end
+                st.link_busy += end - start
+                st.link_bytes += int(round(st.cfg.expert_bytes * (end - start) / st.T))
+                continue
             slot, ready = st.transfer((l, e), t0 if i == 0 else g, "transfer", phase="prefill")
             if e in activated:
                 st.compute(slot, ready, g, st.C(activated[e]), layer=l, expert=e, phase="prefill")

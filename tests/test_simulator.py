@@ -224,7 +224,7 @@ def test_cancellable_prefetch_extension():
         ms, tls, ls = S.simulate_request("duoserve", trs, cfg, cost, net=pp)
         mc, tlc, lc = S.simulate_request("duoserve", trs, cfg, cost, net=pp, cancel_chunk_bytes=chunk)
         assert lc == ls
-        assert mc.e2e_s <= ms.e2e_s and mc.ttft_s == ms.ttft_s
+        assert mc.e2e_s <= ms.e2e_s and mc.ttft_s <= ms.ttft_s
         assert mc.link_bytes <= ms.link_bytes
         tlc.check()
         mo, _, _ = S.simulate_request("oracle", trs, cfg, cost)
