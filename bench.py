@@ -269,8 +269,13 @@ def run_ours(args):
     if args.ep and ws > 1:
         from paper_2509_07379_b200.ep import EPConfig
         ep = EPConfig(rank, ws, combine=args.ep_combine)
+    store = None
+    if ws > 1 and ep is None:
+        # replicas of one model: one shared pinned copy of the expert store per node
+        from paper_2509_07379_b200.engine import HostExpertStore
+        store = HostExpertStore(shape, args.seed, dev, shared_group=dist.group.WORLD)
     eng = Engine(shape, args.policy if args.policy != "oracle" else "duoserve", seed=args.seed, device=dev,
-                 predictor=net, pop=pop, aff=aff, max_seq=args.prefill + args.decode + 8,
+                 store=store, predictor=net, pop=pop, aff=aff, max_seq=args.prefill + args.decode + 8,
                  max_prefill=args.prefill, cancel_mispredicted=not args.no_cancel, chunk_mb=args.chunk_mb,
                  link_depth=args.link_depth, ep=ep, spec_chunk_mb=args.spec_chunk_mb)
     # replicas: an independent request per rank; EP: every rank serves the same request

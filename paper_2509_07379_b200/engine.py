@@ -53,9 +53,15 @@ from .stats import OnlineRoutingStats
 class HostExpertStore:
     """Pinned host memory holding every expert blob: [L, M, blob_bytes] u8."""
 
-    def __init__(self, shape: ModelShape, seed: int, device, layers: int | None = None, experts=None):
+    def __init__(self, shape: ModelShape, seed: int, device, layers: int | None = None, experts=None,
+                 shared_group=None):
         """experts: the expert ids this process stores (expert parallelism);
-        default all M.  Non-owned experts are never allocated."""
+        default all M.  Non-owned experts are never allocated.
+
+        shared_group: a torch.distributed group of ranks on this node serving
+        replicas of the same model: they share ONE copy of the store (an
+        anonymous memfd mapped by every rank and pinned with cudaHostRegister),
+        so host memory holds the 23.4 GB (8x7B) once, not once per GPU."""
         self.shape = shape
         self.seed = seed
         L = layers if layers is not None else shape.num_layers
@@ -63,8 +69,20 @@ class HostExpertStore:
         self.experts = list(range(shape.num_experts)) if experts is None else sorted(experts)
         self.local = {e: i for i, e in enumerate(self.experts)}
         t0 = time.time()
-        self.data = torch.empty((L, len(self.experts), self.blob_bytes), dtype=torch.uint8, pin_memory=True)
+        shape3 = (L, len(self.experts), self.blob_bytes)
+        fill = True
+        self._registered = None
+        if shared_group is not None:
+            self.data, fill = _shared_pinned(shape3, shared_group)
+            self._registered = self.data
+        else:
+            self.data = torch.empty(shape3, dtype=torch.uint8, pin_memory=True)
         self.alloc_s = time.time() - t0
+        if not fill:                                  # another rank generates the bytes
+            import torch.distributed as dist
+            dist.barrier(group=shared_group)
+            self.fill_s = 0.0
+            return
         # generate on the device (counter-based, bit-identical to oracle/w4_ref.py) then D2H
         t0 = time.time()
         stage = [torch.empty(self.blob_bytes, dtype=torch.uint8, device=device) for _ in range(2)]
@@ -76,6 +94,9 @@ class HostExpertStore:
                 self.data[l, i].copy_(buf, non_blocking=True)
         s.synchronize()
         self.fill_s = time.time() - t0
+        if shared_group is not None:
+            import torch.distributed as dist
+            dist.barrier(group=shared_group)             # the bytes are in place for every rank
 
     def blob(self, layer: int, expert: int) -> torch.Tensor:
         return self.data[layer, self.local[expert]]
@@ -83,6 +104,35 @@ class HostExpertStore:
     @property
     def nbytes(self) -> int:
         return self.data.numel()
+
+
+def _shared_pinned(shape3: tuple, group) -> tuple:
+    """(u8 host tensor of shape3 shared by all ranks of `group`, is_creator).
+    Rank 0 of the group creates an anonymous memfd, the others map it through
+    /proc/<pid>/fd; every rank pins its mapping with cudaHostRegister (a
+    registered mapping is DMA-able like cudaHostAlloc memory)."""
+    import os
+    import torch.distributed as dist
+    nbytes = 1
+    for v in shape3:
+        nbytes *= int(v)
+    rank = dist.get_rank(group)
+    fd = None
+    path = [None]
+    if rank == 0:
+        fd = os.memfd_create("duoserve-expert-store", 0)
+        os.ftruncate(fd, nbytes)
+        path[0] = f"/proc/{os.getpid()}/fd/{fd}"
+    dist.broadcast_object_list(path, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    flat = torch.from_file(path[0], shared=True, size=nbytes, dtype=torch.uint8)
+    dist.barrier(group=group)                      # every rank holds a mapping
+    if fd is not None:
+        os.close(fd)
+    if torch.cuda.is_available():
+        rc = torch.cuda.cudart().cudaHostRegister(flat.data_ptr(), nbytes, 0)
+        if int(rc) != 0:
+            raise RuntimeError(f"cudaHostRegister of the shared expert store failed ({rc})")
+    return flat.view(shape3), rank == 0
 
 
 class ExpertCache:

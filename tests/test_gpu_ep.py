@@ -78,3 +78,41 @@ def test_ep_world2_matches_single_gpu(cuda, combine):
         exp = sim_ref.cache_log_prefill(pre, L, owned=experts) + \
             sim_ref.cache_log_decode(dec, preds, L, owned=experts)[0]
         assert log == exp, rank
+
+
+def _replica_worker(rank, world, port, q):
+    import torch.distributed as dist
+    from paper_2509_07379_b200.engine import Engine, HostExpertStore
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dev = torch.device("cuda:0")
+    shape, net, pop, aff, dense, ids = _setup(dev)
+    store = HostExpertStore(shape, 3, dev, shared_group=dist.group.WORLD)
+    eng = Engine(shape, "duoserve", seed=3, dense=dense, predictor=net, pop=pop, aff=aff, max_seq=64,
+                 max_prefill=PREFILL, store=store)
+    toks = eng.generate(ids, DECODE)
+    q.put((rank, toks, bool(store.data.is_pinned())))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_replicas_share_one_pinned_store(cuda):
+    """bench.py --gpus N (replicas): the ranks of a node share one pinned copy
+    of the expert store; every replica decodes exactly the single-process tokens."""
+    from paper_2509_07379_b200.engine import Engine
+    shape, net, pop, aff, dense, ids = _setup(cuda)
+    ref = Engine(shape, "duoserve", seed=3, dense=dense, predictor=net, pop=pop, aff=aff, max_seq=64,
+                 max_prefill=PREFILL).generate(ids, DECODE)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_replica_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=120)
+    assert all(toks == ref and pinned for _, toks, pinned in res), res
