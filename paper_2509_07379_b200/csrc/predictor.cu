@@ -24,6 +24,7 @@
 #include "ds_common.cuh"
 
 #include <cooperative_groups.h>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -204,6 +205,7 @@ __global__ void features_kernel(StateArgs s, int B, double* __restrict__ X) {
 
 // -------------------------------------------------------- fused (B <= 8)
 struct FusedArgs {
+    unsigned long long* dbg;   // optional per-layer globaltimer stamps (DS_K5_TIMELINE), CTA 0
     MlpPlan plan;
     const double* P;
     StateArgs s;
@@ -216,20 +218,25 @@ struct FusedArgs {
     double* probs_out;
 };
 
+// Grid barrier: the CTA's writes are ordered before the arrival by the
+// __syncthreads + a gpu-scope RELEASE add (no full __threadfence, which also
+// invalidates L1), and the spin is an ACQUIRE load; the next layer reads the
+// activations with ld.global.cg (L2), so nothing stale is served from L1.
 __device__ __forceinline__ void grid_barrier(unsigned* counter, unsigned target) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(counter, 1u);
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(counter) : "memory");
         unsigned v;
         do {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter));
-            if (v < target) __nanosleep(64);
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
         } while (v < target);
     }
     __syncthreads();
 }
 
+// BMAX: compile-time bound on the batch (1 for the decode path: no predicated
+// dead lanes of the batch loop in the streaming inner product)
+template <int BMAX>
 __global__ void __launch_bounds__(kFusedThreads, 1) mlp_fused_kernel(FusedArgs a) {
     extern __shared__ __align__(16) double smem[];  // [B][max_width]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -239,50 +246,91 @@ __global__ void __launch_bounds__(kFusedThreads, 1) mlp_fused_kernel(FusedArgs a
     const int B = a.B;
     unsigned phase = 0;
 
-    // phase 0: State Constructor -> act0
-    const int d_in = a.plan.layer[0].in;
-    if (a.X == nullptr) {
-        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * d_in; i += gridDim.x * blockDim.x)
-            a.act0[i] = feature_value(a.s, i / d_in, i % d_in);
-        grid_barrier(a.barrier, ++phase * gridDim.x);
-    }
-    const double* in_act = a.X ? a.X : a.act0;
+    // State Constructor: every CTA builds the (tiny: B x d_in, 81 for 8x7B)
+    // feature rows straight into its shared-memory A stage, so no grid
+    // barrier (and no global round trip) precedes the first layer
+    const bool fused_features = (a.X == nullptr);
+    const double* in_act = a.X;
     double* out_act = a.act1;
 
+    auto stamp = [&](int slot) {
+        if (a.dbg && blockIdx.x == 0 && threadIdx.x == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            a.dbg[slot] = t;
+        }
+    };
+    stamp(0);
     for (int li = 0; li < a.plan.n_layers; ++li) {
         const LayerPtrs& L = a.plan.layer[li];
         const bool last = (li == a.plan.n_layers - 1);
         if (last && blockIdx.x != 0) break;  // output layer: CTA 0 alone
+        stamp(1 + 3 * li);
         // stage A (B x in) in shared memory, L2-coherent loads
-        for (int i = threadIdx.x; i < B * L.in; i += blockDim.x) {
-            int b = i / L.in, c = i % L.in;
-            smem[b * L.ld + c] = __ldcg(in_act + (size_t)b * L.in + c);
+        if (li == 0 && fused_features) {
+            for (int i = threadIdx.x; i < B * L.in; i += blockDim.x) {
+                int b = i / L.in, c = i % L.in;
+                smem[b * L.ld + c] = feature_value(a.s, b, c);
+            }
+        } else {
+            // batched: 8 independent L2 loads per thread in flight, then the stores
+            constexpr int SU = 8;
+            for (int i0 = threadIdx.x; i0 < B * L.in; i0 += blockDim.x * SU) {
+                double v[SU];
+#pragma unroll
+                for (int u = 0; u < SU; ++u) {
+                    const int i = i0 + u * blockDim.x;
+                    if (i < B * L.in) v[u] = __ldcg(in_act + i);   // [B][in] rows are contiguous
+                }
+#pragma unroll
+                for (int u = 0; u < SU; ++u) {
+                    const int i = i0 + u * blockDim.x;
+                    if (i < B * L.in) {
+                        const int b = i / L.in, c = i - b * L.in;
+                        smem[b * L.ld + c] = v[u];
+                    }
+                }
+            }
         }
         if (L.in & 1)
             for (int b = threadIdx.x; b < B; b += blockDim.x) smem[b * L.ld + L.in] = 0.0;
         __syncthreads();
+        stamp(2 + 3 * li);
         const double* W = a.P + L.w;
         const int wstart = last ? warp : gwarp;
         const int wstride = last ? nwarps_cta : nwarps;
         for (int j = wstart; j < L.out; j += wstride) {
-            double acc[kFusedMaxB];
+            double acc[BMAX];
 #pragma unroll
-            for (int b = 0; b < kFusedMaxB; ++b) acc[b] = 0.0;
-            const double* wrow = W + (size_t)j * L.ld;
-#pragma unroll 4
-            for (int c = lane * 2; c < L.ld; c += 64) {
-                double2 w2 = __ldg(reinterpret_cast<const double2*>(wrow + c));
+            for (int b = 0; b < BMAX; ++b) acc[b] = 0.0;
+            const double2* wrow = reinterpret_cast<const double2*>(W + (size_t)j * L.ld);
+            const int n2 = L.ld >> 1;                   // double2 per row (ld is even)
+            // batches of U independent 16-byte loads per lane issued before any
+            // math (a runtime trip count otherwise leaves one load in flight);
+            // each lane still accumulates its elements in increasing c
+            constexpr int U = 8;
+            for (int c0 = lane; c0 < n2; c0 += 32 * U) {
+                double2 w2[U];
 #pragma unroll
-                for (int b = 0; b < kFusedMaxB; ++b) {
-                    if (b < B) {
-                        double2 x2 = *reinterpret_cast<const double2*>(smem + b * L.ld + c);
-                        acc[b] = fma(w2.x, x2.x, acc[b]);
-                        acc[b] = fma(w2.y, x2.y, acc[b]);
+                for (int u = 0; u < U; ++u)
+                    if (c0 + 32 * u < n2) w2[u] = __ldg(wrow + c0 + 32 * u);
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (c0 + 32 * u < n2) {
+                        const int c = 2 * (c0 + 32 * u);
+#pragma unroll
+                        for (int b = 0; b < BMAX; ++b) {
+                            if (b < B) {
+                                double2 x2 = *reinterpret_cast<const double2*>(smem + b * L.ld + c);
+                                acc[b] = fma(w2[u].x, x2.x, acc[b]);
+                                acc[b] = fma(w2[u].y, x2.y, acc[b]);
+                            }
+                        }
                     }
                 }
             }
 #pragma unroll
-            for (int b = 0; b < kFusedMaxB; ++b) {
+            for (int b = 0; b < BMAX; ++b) {
                 if (b < B) {
                     double v = acc[b];
 #pragma unroll
@@ -293,7 +341,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) mlp_fused_kernel(FusedArgs a
             if (lane < B) {
                 double dot = 0.0;
 #pragma unroll
-                for (int b = 0; b < kFusedMaxB; ++b)
+                for (int b = 0; b < BMAX; ++b)
                     if (b == lane) dot = acc[b];
                 double r;
                 if (!last) {
@@ -305,6 +353,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) mlp_fused_kernel(FusedArgs a
                 }
             }
         }
+        stamp(3 + 3 * li);
         if (!last) {
             grid_barrier(a.barrier, ++phase * gridDim.x);
             in_act = out_act;
@@ -407,6 +456,10 @@ int run_forward(const ds_mlp_desc* d, const double* packed, const StateArgs* s, 
 
     if (B <= kFusedMaxB) {
         FusedArgs a;
+        static unsigned long long* dbg = nullptr;
+        static const bool want_dbg = getenv("DS_K5_TIMELINE") != nullptr;
+        if (want_dbg && !dbg) cudaMalloc(&dbg, 64 * sizeof(unsigned long long));
+        a.dbg = want_dbg ? dbg : nullptr;
         a.plan = plan;
         a.P = packed;
         if (s) a.s = *s; else memset(&a.s, 0, sizeof(a.s));
@@ -421,9 +474,12 @@ int run_forward(const ds_mlp_desc* d, const double* packed, const StateArgs* s, 
         int max_ld = 0;
         for (int i = 0; i < plan.n_layers; ++i) max_ld = plan.layer[i].ld > max_ld ? plan.layer[i].ld : max_ld;
         size_t smem = (size_t)B * max_ld * sizeof(double);
+        const void* fn = B == 1 ? (const void*)mlp_fused_kernel<1> : (const void*)mlp_fused_kernel<kFusedMaxB>;
         static bool attr_set = false;
         if (!attr_set) {
-            cudaFuncSetAttribute(mlp_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            cudaFuncSetAttribute(mlp_fused_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            cudaFuncSetAttribute(mlp_fused_kernel<kFusedMaxB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 200 * 1024);
             attr_set = true;
         }
         if (smem > 200 * 1024) return fail(DS_ERR_UNSUPPORTED, "ds_predictor: layer too wide");
@@ -433,13 +489,20 @@ int run_forward(const ds_mlp_desc* d, const double* packed, const StateArgs* s, 
         int grid = num_sms();
         if (cap > 0 && cap < grid) grid = cap;
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mlp_fused_kernel, kFusedThreads, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kFusedThreads, smem);
         if (per_sm < 1) return fail(DS_ERR_UNSUPPORTED, "ds_predictor: fused kernel cannot be resident");
         cudaError_t e = cudaMemsetAsync(barrier, 0, sizeof(unsigned), st);
         if (e != cudaSuccess) return cuda_status(e, "ds_predictor: memset");
         void* args[] = {&a};
-        e = cudaLaunchCooperativeKernel((void*)mlp_fused_kernel, dim3(grid), dim3(kFusedThreads), args,
-                                        smem, st);
+        e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kFusedThreads), args, smem, st);
+        if (want_dbg && e == cudaSuccess) {                  // diagnostics only: per-layer stamps (ns)
+            unsigned long long h[64];
+            cudaStreamSynchronize(st);
+            cudaMemcpy(h, dbg, sizeof(h), cudaMemcpyDeviceToHost);
+            fprintf(stderr, "K5 timeline (us from start):");
+            for (int i = 1; i <= 3 * plan.n_layers; ++i) fprintf(stderr, " %.2f", (h[i] - h[0]) / 1e3);
+            fprintf(stderr, "\n");
+        }
         return cuda_status(e, "ds_predictor: fused launch");
     }
 

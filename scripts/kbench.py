@@ -78,6 +78,25 @@ if "k4" in only:
         if i >= 3:
             tis.append(e0.elapsed_time(e1) / 1e3)
     ti = float(np.median(tis))
+    # same, with one CTA spinning on a side stream during the gap (GPU kept busy)
+    side = torch.cuda.Stream(priority=0)
+    tws = []
+    for i in range(a.iters + 3):
+        torch.cuda.synchronize()
+        with torch.cuda.stream(side):
+            torch.cuda._sleep(int(2.2e6))           # ~1.1 ms at 1.9 GHz, overlapping the gap
+        time.sleep(0.001)
+        s_ = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s_)
+        ops.swiglu_gemv(x, es[i % NB], d, ff, G, h)
+        ops.down_gemv(h, es[i % NB], d, ff, G, rw, 1, acc)
+        e1.record(s_)
+        e1.synchronize()
+        if i >= 3:
+            tws.append(e0.elapsed_time(e1) / 1e3)
+    tw = float(np.median(tws))
+    res["k4_expert_after_busy_gap"] = {"us": tw * 1e6, "GBs": total / tw / 1e9, "frac": total / tw / 1e9 / peaks["hbm_gbs"]}
     res["k4_expert_after_idle"] = {"us": ti * 1e6, "GBs": total / ti / 1e9, "frac": total / ti / 1e9 / peaks["hbm_gbs"]}
 if "k3" in only:
     R = a.rows
