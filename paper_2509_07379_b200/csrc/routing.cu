@@ -34,20 +34,26 @@ __global__ void __launch_bounds__(kGateThreads) gate_topk_kernel(
     const int nvec = d / 8;
     const uint4* xv = reinterpret_cast<const uint4*>(x + (size_t)t * d);
     for (int v = q; v < nvec; v += kGateThreads) {
+        // all M weight vectors and x issued before any math (predicated on
+        // e < M rather than a break, which would serialise the loads)
         uint4 xr = __ldg(xv + v);
+        uint4 wr[kGateMaxM];
+#pragma unroll
+        for (int e = 0; e < kGateMaxM; ++e)
+            if (e < M) wr[e] = __ldg(reinterpret_cast<const uint4*>(wg + (size_t)e * d) + v);
         const uint32_t xs[4] = {xr.x, xr.y, xr.z, xr.w};
 #pragma unroll
         for (int e = 0; e < kGateMaxM; ++e) {
-            if (e >= M) break;
-            uint4 wr = __ldg(reinterpret_cast<const uint4*>(wg + (size_t)e * d) + v);
-            const uint32_t ws[4] = {wr.x, wr.y, wr.z, wr.w};
-            double a = acc[e];
+            if (e < M) {
+                const uint32_t ws[4] = {wr[e].x, wr[e].y, wr[e].z, wr[e].w};
+                double a = acc[e];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                a = fma((double)bf16_lo(xs[i]), (double)bf16_lo(ws[i]), a);
-                a = fma((double)bf16_hi(xs[i]), (double)bf16_hi(ws[i]), a);
+                for (int i = 0; i < 4; ++i) {
+                    a = fma((double)bf16_lo(xs[i]), (double)bf16_lo(ws[i]), a);
+                    a = fma((double)bf16_hi(xs[i]), (double)bf16_hi(ws[i]), a);
+                }
+                acc[e] = a;
             }
-            acc[e] = a;
         }
     }
     for (int e = 0; e < M; ++e) part[e][q] = acc[e];
