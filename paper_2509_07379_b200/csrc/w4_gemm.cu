@@ -80,13 +80,25 @@ template <int NMAT, int TN>
 struct Smem {
     // dequantised weight stages: >= 3 so the dequant of k-tile kt only waits
     // for the MMAs of kt - AS (two k-tiles of tensor-core work of slack)
+    // TN = 128: the dequantised weights (the MMA's A operand) live in TMEM,
+    // written by the dequant warps with tcgen05.st — no shared-memory write of
+    // A and no shared-memory read of A by the tensor core (the 128 x 128 x 16
+    // kind::f16 MMA reading both operands from shared memory needs all of its
+    // 128 B/clk, leaving nothing for the dequant).  TN = 256 needs every TMEM
+    // column for the accumulators, so A stays in shared memory there.
+    static constexpr bool A_TMEM = TN == 128;
     static constexpr int AS = (NMAT == 2 && TN == 256) ? 2 : (NMAT == 2 ? 3 : 4);
-    static constexpr int BS = TN == 256 ? (NMAT == 2 ? 2 : 3) : (NMAT == 2 ? 3 : 4);   // activation stages
+    static constexpr int BS = TN == 256 ? (NMAT == 2 ? 2 : 3) : 4;   // activation stages
     static constexpr int A_STAGE = NMAT * kTileBytes;
     static constexpr int B_STAGE = TN * 128;
     static constexpr int C_STAGE = NMAT * kCodeTile;
     static constexpr int A_OFF = 0;
-    static constexpr int B_OFF = A_OFF + AS * A_STAGE;
+    static constexpr int B_OFF = A_TMEM ? 0 : A_OFF + AS * A_STAGE;
+    // TMEM columns: accumulators [0, NMAT*TN), then (A_TMEM) AS stages of NMAT x 32 columns
+    static constexpr int A_TMEM_COL = NMAT * TN;
+    static constexpr int A_TMEM_STAGE = NMAT * (BK / 2);
+    static constexpr uint32_t TMEM_COLS = A_TMEM ? 512 : NMAT * TN;
+    static_assert(!A_TMEM || A_TMEM_COL + AS * A_TMEM_STAGE <= 512, "TMEM budget");
     static constexpr int C_OFF = B_OFF + BS * B_STAGE;   // code ring: args.code_stages x C_STAGE
     static constexpr int kMaxCS = 8;
     static constexpr int kBarBytes = 512;
@@ -94,6 +106,21 @@ struct Smem {
 };
 
 // Fill the runtime layout of one launch (code stages, staged-scale stride).
+// 32 codes (one uint4) -> 16 bf16x2 words in k order (word w, pair p -> k = 8w + 2p)
+__device__ __forceinline__ void dequant32_regs(const uint4 c, uint32_t zz, uint32_t ss, uint32_t (&o)[16]) {
+    const uint32_t cw[4] = {c.x, c.y, c.z, c.w};
+    const __nv_bfloat162 z2 = *reinterpret_cast<const __nv_bfloat162*>(&zz);
+    const __nv_bfloat162 s2 = *reinterpret_cast<const __nv_bfloat162*>(&ss);
+#pragma unroll
+    for (int w = 0; w < 4; ++w)
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            uint32_t m = nib_pair_magic(cw[w] >> (4 * p));
+            const __nv_bfloat162 v = __hmul2(__hsub2(*reinterpret_cast<const __nv_bfloat162*>(&m), z2), s2);
+            o[4 * w + p] = *reinterpret_cast<const uint32_t*>(&v);   // exact (q-z), one rounding
+        }
+}
+
 template <int NMAT, int TN>
 bool plan_smem(GemmArgs& a) {
     using S = Smem<NMAT, TN>;
@@ -143,7 +170,7 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
     using S = Smem<NMAT, TN>;
     constexpr int AS = S::AS, BS = S::BS;
     const int CS = args.code_stages;
-    constexpr uint32_t TMEM_COLS = NMAT * TN;
+    constexpr uint32_t TMEM_COLS = S::TMEM_COLS;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-B alignment by offsetting the shared array itself (not via an
     // integer round trip) so every derived pointer stays in the shared window
@@ -226,10 +253,17 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
                 for (int kk = 0; kk < BK / UK; ++kk) {
 #pragma unroll
                     for (int j = 0; j < NMAT; ++j) {
-                        const uint64_t adesc = umma_desc_sw128(a_addr + j * kTileBytes);
-                        // advance along K inside the swizzle atom: +32 B = +2 (16-B units)
-                        mma_bf16(tmem_base + j * TN, adesc + 2 * kk, bdesc + 2 * kk, idesc,
-                                 (kt | kk) != 0);
+                        if constexpr (S::A_TMEM) {
+                            // A: lane = weight row, 8 columns (16 bf16) per K step
+                            const uint32_t a_tmem = tmem_base + S::A_TMEM_COL + sa * S::A_TMEM_STAGE +
+                                                    j * (BK / 2) + kk * (UK / 2);
+                            mma_bf16_ts(tmem_base + j * TN, a_tmem, bdesc + 2 * kk, idesc, (kt | kk) != 0);
+                        } else {
+                            const uint64_t adesc = umma_desc_sw128(a_addr + j * kTileBytes);
+                            // advance along K inside the swizzle atom: +32 B = +2 (16-B units)
+                            mma_bf16(tmem_base + j * TN, adesc + 2 * kk, bdesc + 2 * kk, idesc,
+                                     (kt | kk) != 0);
+                        }
                     }
                 }
                 mma_commit(&a_empty[sa]);
@@ -242,7 +276,11 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
         const int td = threadIdx.x - 32 * kFirstDequantWarp;  // 0..511
         const int dg = td >> 8;                  // dequant group: k-tiles kt = 2i + dg (CK = 2)
         const int t = td & 255;
-        const int nl = t >> 1, half = t & 1;     // 2 threads per weight row (32 codes each)
+        // weight row and k-half of this thread: two threads per row (32 codes
+        // each).  With A in TMEM the row must be a lane of this warp's TMEM
+        // quadrant (warp % 4): row = 32 (warp % 4) + lane, half = 4-warp block
+        const int nl = S::A_TMEM ? 32 * (warp & 3) + lane : t >> 1;
+        const int half = S::A_TMEM ? (t >> 7) : (t & 1);
         const int K = args.K, G = args.G;
         const int gpr = K / G;
         const int g0 = kt0 * BK / G;             // first group touching this CTA's k-range
@@ -273,14 +311,30 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
                 const int g = (((kt0 + kt) * BK + 32 * half) >> gshift) - g0;
 #pragma unroll
                 for (int j = 0; j < NMAT; ++j) {
+                    // SWIZZLE_64B code tiles: 16-B chunk u of row r sits at u ^ ((r >> 1) & 3),
+                    // so the 32 rows a warp reads hit distinct banks
+                    const int chunk = (2 * dg + half) ^ ((nl >> 1) & 3);
                     const uint4 c = *reinterpret_cast<const uint4*>(c_tile + j * kCodeTile + nl * (CK * 32) +
-                                                                    dg * 32 + half * 16);
+                                                                    chunk * 16);
                     const uint32_t z = z_s[(j * BM + nl) * ngs + g];
                     const uint32_t zz = (0x4300u | z) * 0x00010001u;
                     const uint32_t ss = (uint32_t)sc_s[(j * BM + nl) * ngs + g] * 0x00010001u;
-                    dequant32(c, zz, ss, a_tile + j * kTileBytes + nl * 128, 4 * half, swz);
+                    if constexpr (S::A_TMEM) {
+                        uint32_t o[16];
+                        dequant32_regs(c, zz, ss, o);
+                        // 16 consecutive columns (32 k) of lane nl: column = k / 2
+                        tmem_st16(tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + S::A_TMEM_COL +
+                                  sa * S::A_TMEM_STAGE + j * (BK / 2) + half * 16, o);
+                    } else {
+                        dequant32(c, zz, ss, a_tile + j * kTileBytes + nl * 128, 4 * half, swz);
+                    }
                 }
-                fence_proxy_async_smem();
+                if constexpr (S::A_TMEM) {
+                    tmem_st_wait();
+                    tc_fence_before();
+                } else {
+                    fence_proxy_async_smem();
+                }
                 mbar_arrive(&a_full[sa]);
             }
             mbar_arrive(&c_empty[cs]);           // both groups release every code stage
@@ -365,7 +419,7 @@ int make_codes_map(CUtensorMap* map, const void* codes, int N, int K) {
     cuuint32_t box[2] = {CK * BK / 2, BM};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(codes), dims, strides, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(DS_ERR_ARG, "cuTensorMapEncodeTiled (codes) failed (%d)", (int)r);
     return DS_OK;
