@@ -62,6 +62,9 @@ if "k4" in only:
     t12 = timeit(lambda i: (ops.swiglu_gemv(x, es[i % NB], d, ff, G, h),
                             ops.down_gemv(h, es[i % NB], d, ff, G, rw, 1, acc)), a.iters)
     res["k4_expert"] = {"us": t12 * 1e6, "GBs": total / t12 / 1e9, "frac": total / t12 / 1e9 / peaks["hbm_gbs"]}
+    # the engine's call: ds_w4_expert_gemv (one cooperative launch for R = 1)
+    tf = timeit(lambda i: ops.expert_gemv(x, es[i % NB], d, ff, G, h, rw, 1, acc), a.iters)
+    res["k4_expert_call"] = {"us": tf * 1e6, "GBs": total / tf / 1e9, "frac": total / tf / 1e9 / peaks["hbm_gbs"]}
     # the serving loop runs K4 after the GPU idled ~1-2 ms waiting on the host link:
     # same unit timed after an idle gap (no L2 flush kernel right before it)
     tis = []
