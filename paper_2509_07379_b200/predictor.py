@@ -21,10 +21,10 @@ What runs where:
     ``DeviceError``.
   * ``construct_input`` is kept on the host for API parity (it is what the
     kernel computes; tests compare both).
-  * Training (predictor.py:234-404) is an offline preprocess and is not
-    part of the serving hot path; ``train`` here delegates to the reference
-    algorithm only if the reference package is importable (see
-    ``train_reference``), otherwise raises.
+  * Training (predictor.py:109-130, 234-404: ``build_training_set``,
+    ``bce_loss``, ``train``, ``gradient_check``, ``TrainReport``) is the
+    offline preprocess; it runs on the GPU in torch float64 (training.py) and
+    is re-exported here under the reference's names.
 """
 
 from __future__ import annotations
@@ -462,3 +462,8 @@ def load_model(path) -> ExpertMLP:
     except KeyError as e:
         raise PredictorError(f"{path}: model container missing array {e}") from e
     return net
+
+
+# training (offline preprocess, predictor.py:109-130, 234-404) runs on the GPU
+# in torch float64: training.py
+from .training import TrainReport, bce_loss, build_training_set, gradient_check, train  # noqa: E402,F401
