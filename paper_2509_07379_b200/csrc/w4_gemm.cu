@@ -87,7 +87,7 @@ struct Smem {
     // 128 B/clk, leaving nothing for the dequant).  TN = 256 needs every TMEM
     // column for the accumulators, so A stays in shared memory there.
     static constexpr bool A_TMEM = TN == 128;
-    static constexpr int AS = (NMAT == 2 && TN == 256) ? 2 : (NMAT == 2 ? 3 : 4);
+    static constexpr int AS = (NMAT == 2 && TN == 256) ? 2 : 4;
     static constexpr int BS = TN == 256 ? (NMAT == 2 ? 2 : 3) : 4;   // activation stages
     static constexpr int A_STAGE = NMAT * kTileBytes;
     static constexpr int B_STAGE = TN * 128;
