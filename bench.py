@@ -51,7 +51,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cancel", action="store_true",
                     help="paper-faithful decode: whole-expert prefetch, no cancellation of wrong prefetches")
-    ap.add_argument("--chunk-mb", type=float, default=8.0)
+    ap.add_argument("--chunk-mb", type=float, default=256.0,
+                    help="chunk size of confirmed transfers (re-fetches, promoted prefetches); >= the expert = whole-expert copies")
     ap.add_argument("--link-depth", type=int, default=2)
     ap.add_argument("--spec-chunk-mb", type=float, default=0.5,
                     help="chunk size of speculative (predicted) prefetches until the gate confirms them")

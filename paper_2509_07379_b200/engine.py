@@ -365,7 +365,7 @@ class Engine:
                  dense: DenseWeights | None = None, store: HostExpertStore | None = None,
                  predictor: ExpertMLP | None = None, pop=None, aff=None, oracle_paths=None,
                  max_seq: int = 2048, max_prefill: int = 2048, cancel_mispredicted: bool = True,
-                 chunk_mb: float = 4.0, link_depth: int = 2, use_graphs: bool = True,
+                 chunk_mb: float = 256.0, link_depth: int = 2, use_graphs: bool = True,
                  ep: EPConfig | None = None, collect_stats: bool = False, spec_chunk_mb: float = 0.5):
         self.shape = shape
         self.policy = SchedulerPolicy(policy)
