@@ -19,7 +19,11 @@
 //     sum_k x_k (q_k - z) s = s * ( sum_k x_k (128+q_k) - (128+z) sum_k x_k ),
 // warp-shuffle reduction, SwiGLU / routing-weight epilogue fused.
 #include "ds_common.cuh"
+#include "sm100.cuh"
 
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -256,6 +260,238 @@ __global__ void __launch_bounds__(kGemvThreads, 2) down_gemv_kernel(
             }
         }
     }
+}
+
+// ------------------------------------------ GEMV v5 (K4, bulk-staged, R = 1)
+// The v2 GEMV keeps its weight stream in registers: each warp issues one
+// batch of 16-byte loads per row and then computes, so the bytes in flight
+// per SM are bounded by the warps that are not computing (DRAM 34 % busy
+// under ncu).  Here one producer thread per CTA streams blocks of RB rows
+// (codes, scales, zero nibbles: all three are row-major, so a row block is
+// three contiguous 1-D bulk copies per matrix) into an S-deep shared-memory
+// ring with cp.async.bulk + mbarrier transaction counts, and 16 consumer
+// warps run the same per-row FHFMA dot product as v2 from shared memory
+// (same chunk order and operations: bit-identical results).  One CTA per SM,
+// ~180 KB of weights in flight per SM independent of compute.
+//
+// Row blocks are handed out by a ticket counter (one atomicAdd per block,
+// prefetched one block ahead by the producer), not by a static split: a CTA
+// that becomes resident late — measured on B200: with one 213 KB CTA per SM
+// the 148th CTA of a grid of 148 started 15 us after the others — or shares
+// its SM with the predictor K5 on another stream takes fewer blocks instead
+// of stretching the kernel.  The producer ends each consumer group's stream
+// with a sentinel block; counters live in a ring of kTicketSlots (one slot
+// per launch, round-robin on the host), reset by the last producer to finish.
+namespace k4s {
+constexpr int kConsumers = 16;
+constexpr int kThreads = 32 * (kConsumers + 1);
+constexpr int kSmemBudget = 220 * 1024;
+constexpr int kTicketSlots = 64;
+
+template <int NMAT, int CPL, int G, int RB>
+struct Geo {
+    static constexpr int K = CPL * 1024;                  // 32 lanes x CPL chunks x 32 codes
+    static constexpr int GPR = K / G;                     // groups per row
+    static constexpr int CODE_B = K / 2;
+    static constexpr int SC_B = GPR * 2;
+    static constexpr int Z_B = (RB * GPR / 2 + 32 + 15) & ~15;   // 16-aligned superset of the rows' nibbles
+    static constexpr int MAT_B = RB * CODE_B + RB * SC_B + Z_B;
+    static constexpr int STAGE_B = NMAT * MAT_B;
+    static constexpr int X_B = (K * 2 + (K / 32) * 4 + 127) & ~127;
+};
+}  // namespace k4s
+
+__device__ unsigned g_k4s_ticket[k4s::kTicketSlots];
+__device__ unsigned g_k4s_done[k4s::kTicketSlots];
+
+// stage_x for the consumer warps only (named barrier 1): all loads of a
+// thread are issued before its shared-memory stores
+template <int K>
+__device__ __forceinline__ void stage_x_consumers(const __nv_bfloat16* __restrict__ x, uint32_t* xs, float* xsum) {
+    constexpr int NT = 32 * k4s::kConsumers;
+    constexpr int UNITS = K / 8;                           // 16-byte units
+    constexpr int PER = (UNITS + NT - 1) / NT;
+    const uint4* xu = reinterpret_cast<const uint4*>(x);
+    uint4 v[PER];
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        const int i = threadIdx.x + j * NT;
+        if (i < UNITS) v[j] = __ldg(xu + i);
+    }
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        const int i = threadIdx.x + j * NT;
+        if (i < UNITS) *reinterpret_cast<uint4*>(xs + swz_unit(i) * 4) = v[j];
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+    for (int i = threadIdx.x; i < K / 32; i += NT) {
+        const uint32_t* p = xs + (size_t)i * 16;
+        float s = 0.f;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) s += bf16_lo(p[j]) + bf16_hi(p[j]);
+        xsum[i] = s;
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+}
+
+template <int NMAT, int CPL, int G, int RB, bool SWIGLU>
+__global__ void __launch_bounds__(k4s::kThreads, 1) staged_gemv_kernel(
+    const __nv_bfloat16* __restrict__ x, W4Ptr wa, W4Ptr wb, int N, int S, __nv_bfloat16* __restrict__ hout,
+    const float* __restrict__ route_w, float* __restrict__ out, unsigned slot_id, unsigned long long* dbg) {
+    using namespace ds::sm100;
+    using Gm = k4s::Geo<NMAT, CPL, G, RB>;
+    constexpr int K = Gm::K, GPR = Gm::GPR;
+    constexpr int CPG_SHIFT = G == 128 ? 2 : 1;
+    constexpr int NG = k4s::kConsumers / RB;              // consumer groups (one stage each)
+    auto stamp = [&](int i) {          // DS_K4_TIMELINE: per-CTA globaltimer stamps (diagnostics only)
+        if (dbg) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            atomicMax(dbg + blockIdx.x * 8 + i, t);
+        }
+    };
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint32_t* xs = reinterpret_cast<uint32_t*>(smem);
+    float* xsum = reinterpret_cast<float*>(smem + K * 2);
+    uint8_t* stages = smem + Gm::X_B;
+    uint64_t* full = reinterpret_cast<uint64_t*>(stages + (size_t)S * Gm::STAGE_B);
+    uint64_t* empty = full + S;
+    int* hdr = reinterpret_cast<int*>(empty + S);         // row block of each ring slot (-1: end of stream)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int T = (N + RB - 1) / RB;                      // row blocks
+    const W4Ptr W[2] = {wa, wb};
+    if (threadIdx.x == 0) {
+        stamp(0);
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], RB);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if constexpr (SWIGLU)
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // the down GEMV may launch early
+
+    if (warp == k4s::kConsumers) {                        // producer
+        if (lane != 0) return;
+        unsigned* tk = g_k4s_ticket + slot_id;
+        const uint64_t pol = l2_evict_first_policy();
+        const int first = (int)atomicAdd(tk, (unsigned)S);   // the first S blocks in one grab
+        int pending = -1;
+        int sentinels = 0;
+        for (int s = 0; sentinels < NG; ++s) {
+            const int slot = s % S;
+            if (s >= S) mbar_wait(&empty[slot], ((s / S) - 1) & 1);
+            int t;
+            if (s < S) {
+                t = first + s;
+            } else {
+                t = pending;
+            }
+            if (s >= S - 1 && t < T) pending = (int)atomicAdd(tk, 1u);   // next block, latency hidden
+            if (t >= T || t < 0) t = -1;
+            hdr[slot] = t;
+            if (t < 0) {
+                mbar_arrive(&full[slot]);
+                ++sentinels;
+                continue;
+            }
+            const int r0 = t * RB, rows = min(RB, N - r0);
+            uint8_t* dst = stages + (size_t)slot * Gm::STAGE_B;
+            const uint32_t zb0 = ((uint32_t)(r0 * GPR) >> 1) & ~15u;
+            const uint32_t zb1 = (((uint32_t)((r0 + rows) * GPR) >> 1) + 15u) & ~15u;
+            const uint32_t cb = rows * Gm::CODE_B, sb = rows * Gm::SC_B, zb = zb1 - zb0;
+            mbar_expect_tx(&full[slot], NMAT * (cb + sb + zb));
+#pragma unroll
+            for (int m = 0; m < NMAT; ++m) {
+                uint8_t* md = dst + m * Gm::MAT_B;
+                bulk_load(md, reinterpret_cast<const uint8_t*>(W[m].codes) + (size_t)r0 * Gm::CODE_B, cb, &full[slot],
+                          pol);
+                bulk_load(md + RB * Gm::CODE_B, reinterpret_cast<const uint8_t*>(W[m].scales) + (size_t)r0 * Gm::SC_B,
+                          sb, &full[slot], pol);
+                bulk_load(md + RB * (Gm::CODE_B + Gm::SC_B), W[m].zeros + zb0, zb, &full[slot], pol);
+            }
+            if (s == 0) stamp(1);
+        }
+        stamp(3);
+        __threadfence();                                   // every ticket of this CTA is taken
+        if (atomicAdd(g_k4s_done + slot_id, 1u) == gridDim.x - 1) {
+            atomicExch(tk, 0u);
+            atomicExch(g_k4s_done + slot_id, 0u);
+        }
+        return;
+    }
+
+    if constexpr (!SWIGLU)
+        asm volatile("griddepcontrol.wait;" ::: "memory");   // h comes from the SwiGLU GEMV (PDL launch)
+    stage_x_consumers<K>(x, xs, xsum);
+    if (threadIdx.x == 0) stamp(2);
+    const int grp = warp / RB, r = warp % RB;
+    bool first_stage = true;
+    for (int s = grp;; s += NG) {
+        const int slot = s % S;
+        mbar_wait(&full[slot], (s / S) & 1);
+        const int t = hdr[slot];
+        if (t < 0) break;                                  // end of this group's stream
+        if (first_stage && lane == 0) stamp(4);
+        first_stage = false;
+        const int r0 = t * RB;
+        const int n = r0 + r;
+        if (n < N) {
+            const uint8_t* base = stages + (size_t)slot * Gm::STAGE_B;
+            const uint32_t zb0 = ((uint32_t)(r0 * GPR) >> 1) & ~15u;
+            float acc[NMAT];
+#pragma unroll
+            for (int m = 0; m < NMAT; ++m) acc[m] = 0.f;
+#pragma unroll
+            for (int i = 0; i < CPL; ++i) {
+                const int c = lane + 32 * i;
+                const int g = c >> CPG_SHIFT;
+                const int sw = (c >> 1) & 3;
+                const uint32_t* xc = xs + (c << 4);
+                const float xsm = xsum[c];
+                uint4 xv[4];
+#pragma unroll
+                for (int ii = 0; ii < 4; ++ii) xv[ii] = *reinterpret_cast<const uint4*>(xc + 4 * (ii ^ sw));
+                const uint32_t zn = (uint32_t)(n * GPR + g);          // global nibble index of the zero
+#pragma unroll
+                for (int m = 0; m < NMAT; ++m) {
+                    const uint8_t* mb = base + m * Gm::MAT_B;
+                    const uint4 c4 = *reinterpret_cast<const uint4*>(mb + r * Gm::CODE_B + c * 16);
+                    const uint16_t sv = reinterpret_cast<const uint16_t*>(mb + RB * Gm::CODE_B + r * Gm::SC_B)[g];
+                    const uint8_t zv = mb[RB * (Gm::CODE_B + Gm::SC_B) + (zn >> 1) - zb0];
+                    const uint32_t cw[4] = {c4.x, c4.y, c4.z, c4.w};
+                    float p[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                    for (int ii = 0; ii < 4; ++ii) {
+                        const uint32_t xx[4] = {xv[ii].x, xv[ii].y, xv[ii].z, xv[ii].w};
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const uint32_t pr = nib_pair_magic(cw[ii] >> (4 * q));
+                            fma_bf16_lo(p[(q & 1) * 2], pr, xx[q]);
+                            fma_bf16_hi(p[(q & 1) * 2 + 1], pr, xx[q]);
+                        }
+                    }
+                    const float z128 = __uint_as_float(0x43000000u | ((((uint32_t)zv >> ((zn & 1) << 2)) & 15u) << 16));
+                    const float sc = __uint_as_float((uint32_t)sv << 16);
+                    acc[m] = fmaf(sc, ((p[0] + p[1]) + (p[2] + p[3])) - z128 * xsm, acc[m]);
+                }
+            }
+#pragma unroll
+            for (int m = 0; m < NMAT; ++m) acc[m] = warp_sum(acc[m]);
+            if (lane == 0) {
+                if constexpr (SWIGLU) {
+                    const float av = acc[0], bv = acc[NMAT - 1];
+                    hout[n] = __float2bfloat16_rn(av / (1.0f + expf(-av)) * bv);
+                } else {
+                    out[n] = __fadd_rn(out[n], __fmul_rn(route_w[0], acc[0]));
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+    }
+    if (lane == 0) stamp(5);
 }
 
 // ------------------------------------------------- GEMV v3 (K4, mma.sync)
@@ -696,11 +932,126 @@ static int down_launch_u(const __nv_bfloat16* h, const ds_w4_expert* e, int d, i
     return DS_OK;
 }
 
+// v5 (bulk-staged) launchers; return 1 when the shape has no staged
+// instantiation (the caller falls back to v2).  DS_K4_VARIANT=v2|mma forces
+// the older variants (A/B runs).
+// one ticket slot per launch, shared by every instantiation (a SwiGLU GEMV and
+// the PDL down GEMV that overlaps it must not share a counter)
+inline unsigned k4s_next_slot() {
+    static std::atomic<unsigned> seq{0};
+    return seq.fetch_add(1, std::memory_order_relaxed) % k4s::kTicketSlots;
+}
+
+inline bool k4_staged_enabled() {
+    static const char* v = getenv("DS_K4_VARIANT");
+    return !(v && (v[0] == 'v' || v[0] == 'm'));
+}
+
+template <int NMAT, int CPL, int G, int RB, bool SWIGLU>
+static int staged_launch(const __nv_bfloat16* x, W4Ptr a, W4Ptr b, int N, __nv_bfloat16* hout, const float* rw,
+                         float* out, cudaStream_t st) {
+    using Gm = k4s::Geo<NMAT, CPL, G, RB>;
+    static int S = -1;
+    static size_t smem = 0;
+    if (S < 0) {
+        int s_ = (k4s::kSmemBudget - Gm::X_B) / (Gm::STAGE_B + 20);
+        if (s_ > 8) s_ = 8;
+        smem = (size_t)Gm::X_B + (size_t)s_ * Gm::STAGE_B + 20 * (size_t)s_;
+        if (s_ >= 2)
+            cudaFuncSetAttribute(staged_gemv_kernel<NMAT, CPL, G, RB, SWIGLU>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        S = s_;
+    }
+    if (S < 2 || S < k4s::kConsumers / RB) return 1;   // every consumer group needs its own slot
+    static const int gcap = getenv("DS_K4S_GRID") ? atoi(getenv("DS_K4S_GRID")) : 0;   // A/B runs
+    int grid = N < num_sms() ? N : num_sms();
+    if (gcap > 0 && gcap < grid) grid = gcap;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(k4s::kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];   // down: PDL launch, its first stages stream during the SwiGLU tail
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = SWIGLU ? 0 : 1;
+    static const bool want_dbg = getenv("DS_K4_TIMELINE") != nullptr;
+    static unsigned long long* dbg = nullptr;
+    if (want_dbg && !dbg) cudaMalloc(&dbg, 8 * 1024 * sizeof(unsigned long long));
+    if (want_dbg) cudaMemsetAsync(dbg, 0, 8 * 1024 * sizeof(unsigned long long), st);
+    const unsigned slot_id = k4s_next_slot();
+    cudaLaunchKernelEx(&cfg, staged_gemv_kernel<NMAT, CPL, G, RB, SWIGLU>, x, a, b, N, S, hout, rw, out, slot_id,
+                       want_dbg ? dbg : nullptr);
+    DS_LAUNCH_CHECK(SWIGLU ? "ds_w4_swiglu_gemv (staged)" : "ds_w4_down_gemv (staged)");
+    if (want_dbg) {      // diagnostics only: per-CTA stamps (us from the earliest CTA entry)
+        static unsigned long long h[8 * 1024];
+        cudaStreamSynchronize(st);
+        cudaMemcpy(h, dbg, 8 * grid * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+        unsigned long long t0 = ~0ull;
+        for (int b = 0; b < grid; ++b) t0 = h[8 * b] < t0 ? h[8 * b] : t0;
+        const char* names[6] = {"entry", "issued", "x_staged", "producer_done", "first_stage", "consumer_done"};
+        fprintf(stderr, "K4 staged %s timeline (us, min/median/max over %d CTAs):", SWIGLU ? "swiglu" : "down", grid);
+        for (int i = 0; i < 6; ++i) {
+            double v[1024];
+            int n = 0;
+            for (int b = 0; b < grid; ++b)
+                if (h[8 * b + i]) v[n++] = (h[8 * b + i] - t0) / 1e3;
+            std::sort(v, v + n);
+            if (n) fprintf(stderr, " %s %.2f/%.2f/%.2f", names[i], v[0], v[n / 2], v[n - 1]);
+        }
+        fprintf(stderr, " late:");
+        for (int b = 0; b < grid; ++b)
+            if (h[8 * b] - t0 > 2000) fprintf(stderr, " %d(%.1f)", b, (h[8 * b] - t0) / 1e3);
+        fprintf(stderr, "\n");
+    }
+    return DS_OK;
+}
+
+template <int G>
+static bool staged_shape_ok(int K, int N) {
+    const int gpr = K / G;   // scale rows 16-B aligned, zero-nibble array a multiple of 16 B
+    return K % 1024 == 0 && gpr % 8 == 0 && ((long long)N * gpr) % 32 == 0 && N > 0;
+}
+
+template <int G>
+static int swiglu_staged(const __nv_bfloat16* x, const ds_w4_expert* e, int d, int ff, __nv_bfloat16* h,
+                         cudaStream_t st) {
+    if (!k4_staged_enabled() || !staged_shape_ok<G>(d, ff)) return 1;
+    static const int rb = getenv("DS_K4S_RB_UP") ? atoi(getenv("DS_K4S_RB_UP")) : 8;   // A/B runs
+#define DS_SW(CPL, RB) staged_launch<2, CPL, G, RB, true>(x, to_ptr(e->w1), to_ptr(e->w3), ff, h, nullptr, nullptr, st)
+    switch (d / 1024) {
+        case 4: return rb == 4 ? DS_SW(4, 4) : rb == 16 ? DS_SW(4, 16) : DS_SW(4, 8);
+        case 6: return rb == 4 ? DS_SW(6, 4) : rb == 16 ? DS_SW(6, 16) : DS_SW(6, 8);
+        default: return 1;
+    }
+#undef DS_SW
+}
+
+template <int G>
+static int down_staged(const __nv_bfloat16* h, const ds_w4_expert* e, int d, int ff, const float* rw, float* acc,
+                       cudaStream_t st) {
+    if (!k4_staged_enabled() || !staged_shape_ok<G>(ff, d)) return 1;
+    static const int rb = getenv("DS_K4S_RB_DOWN") ? atoi(getenv("DS_K4S_RB_DOWN")) : 4;   // A/B runs
+    if (rb == 0) return 1;                                                                   // v2 down
+#define DS_DN(CPL, RB) staged_launch<1, CPL, G, RB, false>(h, to_ptr(e->w2), to_ptr(e->w2), d, nullptr, rw, acc, st)
+    switch (ff / 1024) {
+        case 14: return rb == 2 ? DS_DN(14, 2) : rb == 8 ? DS_DN(14, 8) : DS_DN(14, 4);
+        case 16: return rb == 2 ? DS_DN(16, 2) : rb == 8 ? DS_DN(16, 8) : DS_DN(16, 4);
+        default: return 1;
+    }
+#undef DS_DN
+}
+
 // batch size per lane U (16-byte loads in flight per matrix) chosen so that
 // (K/32)/32 is a multiple of U: no predicates in the streaming loop
 template <int R, int G>
 static int swiglu_launch_g(const __nv_bfloat16* x, const ds_w4_expert* e, int d, int ff, __nv_bfloat16* h,
                            cudaStream_t st) {
+    if constexpr (R == 1) {
+        const int rc = swiglu_staged<G>(x, e, d, ff, h, st);
+        if (rc <= 0) return rc;
+    }
     const int per_lane = (d / 32) % 32 == 0 ? (d / 32) / 32 : 0;
     if (per_lane && per_lane % 4 == 0) return swiglu_launch_u<R, G, 4, false>(x, e, d, ff, h, st);
     if (per_lane && per_lane % 3 == 0) return swiglu_launch_u<R, G, 3, false>(x, e, d, ff, h, st);
@@ -711,6 +1062,10 @@ static int swiglu_launch_g(const __nv_bfloat16* x, const ds_w4_expert* e, int d,
 template <int R, int G>
 static int down_launch_g(const __nv_bfloat16* h, const ds_w4_expert* e, int d, int ff, const float* rw, int rs,
                          float* acc, cudaStream_t st) {
+    if constexpr (R == 1) {
+        const int rc = down_staged<G>(h, e, d, ff, rw, acc, st);
+        if (rc <= 0) return rc;
+    }
     const int per_lane = (ff / 32) % 32 == 0 ? (ff / 32) / 32 : 0;
     if (per_lane && per_lane % 8 == 0) return down_launch_u<R, G, 8, false>(h, e, d, ff, rw, rs, acc, st);
     if (per_lane && per_lane % 7 == 0) return down_launch_u<R, G, 7, false>(h, e, d, ff, rw, rs, acc, st);

@@ -62,6 +62,12 @@ if "k4" in only:
     t12 = timeit(lambda i: (ops.swiglu_gemv(x, es[i % NB], d, ff, G, h),
                             ops.down_gemv(h, es[i % NB], d, ff, G, rw, 1, acc)), a.iters)
     res["k4_expert"] = {"us": t12 * 1e6, "GBs": total / t12 / 1e9, "frac": total / t12 / 1e9 / peaks["hbm_gbs"]}
+    # back to back without the flush kernel in between (4 experts x 91.5 MB cycle through a 126 MB L2,
+    # so the weights are still cold); the flush kernel's different shared-memory carveout is not in front
+    t12n = timeit(lambda i: (ops.swiglu_gemv(x, es[i % NB], d, ff, G, h),
+                             ops.down_gemv(h, es[i % NB], d, ff, G, rw, 1, acc)), a.iters, flush_l2=False)
+    res["k4_expert_noflush"] = {"us": t12n * 1e6, "GBs": total / t12n / 1e9,
+                                "frac": total / t12n / 1e9 / peaks["hbm_gbs"]}
     # the engine's call: ds_w4_expert_gemv (one cooperative launch for R = 1)
     tf = timeit(lambda i: ops.expert_gemv(x, es[i % NB], d, ff, G, h, rw, 1, acc), a.iters)
     res["k4_expert_call"] = {"us": tf * 1e6, "GBs": total / tf / 1e9, "frac": total / tf / 1e9 / peaks["hbm_gbs"]}

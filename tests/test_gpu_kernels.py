@@ -121,6 +121,7 @@ def test_w4_dequant_bit_exact(cuda):
 
 
 @pytest.mark.parametrize("d,ff,R,G", [(256, 896, 1, 128), (4096, 14336, 1, 128), (4096, 14336, 3, 128),
+                                      (4096, 14336, 1, 64), (6144, 16384, 1, 64),
                                       (6144, 16384, 1, 128), (256, 896, 6, 128), (4096, 14336, 8, 128),
                                       (256, 896, 11, 128), (512, 1024, 3, 64), (256, 896, 5, 64)])
 def test_w4_gemv_vs_f64_reference(d, ff, R, G, cuda):
