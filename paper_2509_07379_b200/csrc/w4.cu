@@ -334,6 +334,65 @@ __device__ __forceinline__ void stage_x_consumers(const __nv_bfloat16* __restric
     asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
 }
 
+// The producer thread of a bulk-staged GEMV CTA: takes row blocks from the
+// ticket counter, streams each into the next ring slot, and ends every
+// consumer group's stream with a sentinel block (hdr = -1).
+template <int NMAT, int CPL, int G, int RB>
+__device__ __forceinline__ void k4s_produce(const W4Ptr (&W)[2], int N, int S, int NG, uint8_t* stages, uint64_t* full,
+                                            uint64_t* empty, int* hdr, unsigned slot_id, unsigned long long* dbg) {
+    using namespace ds::sm100;
+    using Gm = k4s::Geo<NMAT, CPL, G, RB>;
+    constexpr int GPR = Gm::GPR;
+    const int T = (N + RB - 1) / RB;
+    unsigned* tk = g_k4s_ticket + slot_id;
+    const uint64_t pol = l2_evict_first_policy();
+    const int first = (int)atomicAdd(tk, (unsigned)S);   // the first S blocks in one grab
+    int pending = -1;
+    int sentinels = 0;
+    for (int s = 0; sentinels < NG; ++s) {
+        const int slot = s % S;
+        if (s >= S) mbar_wait(&empty[slot], ((s / S) - 1) & 1);
+        int t = s < S ? first + s : pending;
+        if (s >= S - 1 && t < T) pending = (int)atomicAdd(tk, 1u);   // next block, latency hidden
+        if (t >= T || t < 0) t = -1;
+        hdr[slot] = t;
+        if (t < 0) {
+            mbar_arrive(&full[slot]);
+            ++sentinels;
+            continue;
+        }
+        const int r0 = t * RB, rows = min(RB, N - r0);
+        uint8_t* dst = stages + (size_t)slot * Gm::STAGE_B;
+        const uint32_t zb0 = ((uint32_t)(r0 * GPR) >> 1) & ~15u;
+        const uint32_t zb1 = (((uint32_t)((r0 + rows) * GPR) >> 1) + 15u) & ~15u;
+        const uint32_t cb = rows * Gm::CODE_B, sb = rows * Gm::SC_B, zb = zb1 - zb0;
+        mbar_expect_tx(&full[slot], NMAT * (cb + sb + zb));
+#pragma unroll
+        for (int m = 0; m < NMAT; ++m) {
+            uint8_t* md = dst + m * Gm::MAT_B;
+            bulk_load(md, reinterpret_cast<const uint8_t*>(W[m].codes) + (size_t)r0 * Gm::CODE_B, cb, &full[slot], pol);
+            bulk_load(md + RB * Gm::CODE_B, reinterpret_cast<const uint8_t*>(W[m].scales) + (size_t)r0 * Gm::SC_B, sb,
+                      &full[slot], pol);
+            bulk_load(md + RB * (Gm::CODE_B + Gm::SC_B), W[m].zeros + zb0, zb, &full[slot], pol);
+        }
+        if (s == 0 && dbg) {
+            unsigned long long ts;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
+            atomicMax(dbg + blockIdx.x * 8 + 1, ts);
+        }
+    }
+    if (dbg) {
+        unsigned long long ts;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
+        atomicMax(dbg + blockIdx.x * 8 + 3, ts);
+    }
+    __threadfence();                                       // every ticket of this CTA is taken
+    if (atomicAdd(g_k4s_done + slot_id, 1u) == gridDim.x - 1) {
+        atomicExch(tk, 0u);
+        atomicExch(g_k4s_done + slot_id, 0u);
+    }
+}
+
 template <int NMAT, int CPL, int G, int RB, bool SWIGLU>
 __global__ void __launch_bounds__(k4s::kThreads, 1) staged_gemv_kernel(
     const __nv_bfloat16* __restrict__ x, W4Ptr wa, W4Ptr wb, int N, int S, __nv_bfloat16* __restrict__ hout,
@@ -373,52 +432,8 @@ __global__ void __launch_bounds__(k4s::kThreads, 1) staged_gemv_kernel(
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // the down GEMV may launch early
 
     if (warp == k4s::kConsumers) {                        // producer
-        if (lane != 0) return;
-        unsigned* tk = g_k4s_ticket + slot_id;
-        const uint64_t pol = l2_evict_first_policy();
-        const int first = (int)atomicAdd(tk, (unsigned)S);   // the first S blocks in one grab
-        int pending = -1;
-        int sentinels = 0;
-        for (int s = 0; sentinels < NG; ++s) {
-            const int slot = s % S;
-            if (s >= S) mbar_wait(&empty[slot], ((s / S) - 1) & 1);
-            int t;
-            if (s < S) {
-                t = first + s;
-            } else {
-                t = pending;
-            }
-            if (s >= S - 1 && t < T) pending = (int)atomicAdd(tk, 1u);   // next block, latency hidden
-            if (t >= T || t < 0) t = -1;
-            hdr[slot] = t;
-            if (t < 0) {
-                mbar_arrive(&full[slot]);
-                ++sentinels;
-                continue;
-            }
-            const int r0 = t * RB, rows = min(RB, N - r0);
-            uint8_t* dst = stages + (size_t)slot * Gm::STAGE_B;
-            const uint32_t zb0 = ((uint32_t)(r0 * GPR) >> 1) & ~15u;
-            const uint32_t zb1 = (((uint32_t)((r0 + rows) * GPR) >> 1) + 15u) & ~15u;
-            const uint32_t cb = rows * Gm::CODE_B, sb = rows * Gm::SC_B, zb = zb1 - zb0;
-            mbar_expect_tx(&full[slot], NMAT * (cb + sb + zb));
-#pragma unroll
-            for (int m = 0; m < NMAT; ++m) {
-                uint8_t* md = dst + m * Gm::MAT_B;
-                bulk_load(md, reinterpret_cast<const uint8_t*>(W[m].codes) + (size_t)r0 * Gm::CODE_B, cb, &full[slot],
-                          pol);
-                bulk_load(md + RB * Gm::CODE_B, reinterpret_cast<const uint8_t*>(W[m].scales) + (size_t)r0 * Gm::SC_B,
-                          sb, &full[slot], pol);
-                bulk_load(md + RB * (Gm::CODE_B + Gm::SC_B), W[m].zeros + zb0, zb, &full[slot], pol);
-            }
-            if (s == 0) stamp(1);
-        }
-        stamp(3);
-        __threadfence();                                   // every ticket of this CTA is taken
-        if (atomicAdd(g_k4s_done + slot_id, 1u) == gridDim.x - 1) {
-            atomicExch(tk, 0u);
-            atomicExch(g_k4s_done + slot_id, 0u);
-        }
+        if (lane == 0)
+            k4s_produce<NMAT, CPL, G, RB>(W, N, S, NG, stages, full, empty, hdr, slot_id, dbg);
         return;
     }
 
@@ -942,6 +957,202 @@ inline unsigned k4s_next_slot() {
     return seq.fetch_add(1, std::memory_order_relaxed) % k4s::kTicketSlots;
 }
 
+// v5 SwiGLU GEMV with the tensor cores (G = 128, R = 1): the same producer /
+// ring / ticket structure with 16-row blocks; the 16 consumer warps form two
+// groups of 8, a group takes a block and splits K: warp w of the group owns
+// quantisation groups [w*GPR/8, (w+1)*GPR/8) of all 16 rows.  Per group,
+// lane (g, t) dequantises code chunk t of rows g and g+8 straight into
+// mma.m16n8k16 A fragments (v3's mapping: 8 mmas per matrix per group, the k
+// permutation inside an mma applied to x as well), x (unswizzled in shared
+// memory) gives the B fragments, and the group scale is factored out with a
+// precomputed per-group sum of x:  s * (D - (128 + z) * sum_group x).  With
+// one activation row every D column holds the same dot product.  The 8
+// partial sums per row are reduced through shared memory in a fixed order
+// (deterministic); 2.3x fewer issue slots per weight than the FHFMA
+// consumer, which is issue-bound on the SwiGLU half.
+template <int CPL>
+__global__ void __launch_bounds__(k4s::kThreads, 1) staged_mma_swiglu_kernel(
+    const __nv_bfloat16* __restrict__ x, W4Ptr wa, W4Ptr wb, int N, int S, __nv_bfloat16* __restrict__ hout,
+    unsigned slot_id, unsigned long long* dbg) {
+    using namespace ds::sm100;
+    constexpr int NMAT = 2, G = 128, RB = 16;
+    using Gm = k4s::Geo<NMAT, CPL, G, RB>;
+    constexpr int K = Gm::K, GPR = Gm::GPR;
+    constexpr int WPG = 8;                                  // warps per block (K split)
+    constexpr int NG = k4s::kConsumers / WPG;               // consumer groups
+    constexpr int GPW = GPR / WPG;                          // quantisation groups per warp
+    constexpr int XB = (K * 2 + GPR * 4 + 127) & ~127;
+    static_assert(GPR % WPG == 0, "K split must be whole groups");
+    extern __shared__ __align__(128) uint8_t smem[];
+    const __nv_bfloat16* xs = reinterpret_cast<const __nv_bfloat16*>(smem);
+    float* xgs = reinterpret_cast<float*>(smem + K * 2);   // sum of x per quantisation group
+    uint8_t* stages = smem + XB;
+    uint64_t* full = reinterpret_cast<uint64_t*>(stages + (size_t)S * Gm::STAGE_B);
+    uint64_t* empty = full + S;
+    int* hdr = reinterpret_cast<int*>(empty + S);
+    float* red = reinterpret_cast<float*>(hdr + ((S + 3) & ~3));   // [2 parity][NG][WPG][NMAT][16]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const W4Ptr W[2] = {wa, wb};
+    if (threadIdx.x == 0) {
+        if (dbg) {
+            unsigned long long ts;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
+            atomicMax(dbg + blockIdx.x * 8, ts);
+        }
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], WPG);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // the down GEMV may launch early
+    if (warp == k4s::kConsumers) {
+        if (lane == 0) k4s_produce<NMAT, CPL, G, RB>(W, N, S, NG, stages, full, empty, hdr, slot_id, dbg);
+        return;
+    }
+    {   // x -> shared memory (plain layout), then the per-group sums (one warp per group)
+        constexpr int NT = 32 * k4s::kConsumers;
+        constexpr int UNITS = K / 8;
+        constexpr int PER = (UNITS + NT - 1) / NT;
+        const uint4* xu = reinterpret_cast<const uint4*>(x);
+        uint4 v[PER];
+#pragma unroll
+        for (int j = 0; j < PER; ++j)
+            if (threadIdx.x + j * NT < UNITS) v[j] = __ldg(xu + threadIdx.x + j * NT);
+#pragma unroll
+        for (int j = 0; j < PER; ++j)
+            if (threadIdx.x + j * NT < UNITS) reinterpret_cast<uint4*>(smem)[threadIdx.x + j * NT] = v[j];
+        asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+        for (int j = warp; j < GPR; j += k4s::kConsumers) {
+            const uint32_t* p = reinterpret_cast<const uint32_t*>(xs + 128 * j) + 2 * lane;
+            float s_ = (bf16_lo(p[0]) + bf16_hi(p[0])) + (bf16_lo(p[1]) + bf16_hi(p[1]));
+            s_ = warp_sum(s_);
+            if (lane == 0) xgs[j] = s_;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+    }
+    const int grp = warp / WPG, wk = warp % WPG;
+    const int g = lane >> 2, t = lane & 3;
+    for (int s = grp, it = 0;; s += NG, ++it) {
+        const int slot = s % S;
+        mbar_wait(&full[slot], (s / S) & 1);
+        const int tb = hdr[slot];
+        if (tb < 0) break;                                  // end of this group's stream
+        const int r0 = tb * RB;
+        const uint8_t* base = stages + (size_t)slot * Gm::STAGE_B;
+        const uint32_t zb0 = ((uint32_t)(r0 * GPR) >> 1) & ~15u;
+        float acc[NMAT][2] = {};
+#pragma unroll
+        for (int jj = 0; jj < GPW; ++jj) {
+            const int j = wk * GPW + jj;
+            uint4 xv[4];
+            const uint4* xp = reinterpret_cast<const uint4*>(xs + 128 * j + 32 * t);
+#pragma unroll
+            for (int w = 0; w < 4; ++w) xv[w] = xp[w];
+            uint4 c[NMAT][2];
+#pragma unroll
+            for (int m = 0; m < NMAT; ++m)
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh)
+                    c[m][hh] = *reinterpret_cast<const uint4*>(base + m * Gm::MAT_B + (g + 8 * hh) * Gm::CODE_B +
+                                                               (4 * j + t) * 16);
+            float d[NMAT][4] = {};
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+                const uint32_t xw[4] = {xv[w].x, xv[w].y, xv[w].z, xv[w].w};
+#pragma unroll
+                for (int s2 = 0; s2 < 2; ++s2) {
+#pragma unroll
+                    for (int m = 0; m < NMAT; ++m) {
+                        const uint32_t* cg = reinterpret_cast<const uint32_t*>(&c[m][0]);
+                        const uint32_t* cg8 = reinterpret_cast<const uint32_t*>(&c[m][1]);
+                        mma16816(d[m], nib_pair_magic(cg[w] >> (8 * s2)), nib_pair_magic(cg8[w] >> (8 * s2)),
+                                 nib_pair_magic(cg[w] >> (8 * s2 + 4)), nib_pair_magic(cg8[w] >> (8 * s2 + 4)),
+                                 xw[2 * s2], xw[2 * s2 + 1]);
+                    }
+                }
+            }
+            const float xg = xgs[j];
+#pragma unroll
+            for (int m = 0; m < NMAT; ++m) {
+                const uint8_t* mb = base + m * Gm::MAT_B;
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    const int row = g + 8 * hh;
+                    const uint16_t sv = reinterpret_cast<const uint16_t*>(mb + RB * Gm::CODE_B + row * Gm::SC_B)[j];
+                    const uint32_t zn = (uint32_t)((r0 + row) * GPR + j);
+                    const uint32_t zq = ((uint32_t)mb[RB * (Gm::CODE_B + Gm::SC_B) + (zn >> 1) - zb0] >> ((zn & 1) << 2)) & 15u;
+                    const float z128 = __uint_as_float(0x43000000u | (zq << 16));
+                    const float sc = __uint_as_float((uint32_t)sv << 16);
+                    acc[m][hh] = fmaf(sc, fmaf(-z128, xg, d[m][2 * hh]), acc[m][hh]);
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);           // the block's bytes are consumed
+        float* rd = red + (size_t)((it & 1) * NG + grp) * WPG * NMAT * 16;
+        if (t == 0) {
+#pragma unroll
+            for (int m = 0; m < NMAT; ++m) {
+                rd[(wk * NMAT + m) * 16 + g] = acc[m][0];
+                rd[(wk * NMAT + m) * 16 + g + 8] = acc[m][1];
+            }
+        }
+        asm volatile("bar.sync %0, %1;" ::"r"(2 + grp), "n"(32 * WPG) : "memory");
+        if (wk == 0 && lane < 16) {
+            float av = 0.f, bv = 0.f;
+#pragma unroll
+            for (int w = 0; w < WPG; ++w) {
+                av += rd[(w * NMAT + 0) * 16 + lane];
+                bv += rd[(w * NMAT + 1) * 16 + lane];
+            }
+            const int n = r0 + lane;
+            if (n < N) hout[n] = __float2bfloat16_rn(av / (1.0f + expf(-av)) * bv);
+        }
+    }
+}
+
+template <int CPL>
+static int staged_mma_launch(const __nv_bfloat16* x, W4Ptr a, W4Ptr b, int N, __nv_bfloat16* hout, cudaStream_t st) {
+    using Gm = k4s::Geo<2, CPL, 128, 16>;
+    constexpr int XB = (Gm::K * 2 + Gm::GPR * 4 + 127) & ~127;
+    constexpr int RED = 2 * 2 * 8 * 2 * 16 * 4;
+    static int S = -1;
+    static size_t smem = 0;
+    if (S < 0) {
+        int s_ = (k4s::kSmemBudget - XB - RED - 16) / (Gm::STAGE_B + 20);
+        if (s_ > 8) s_ = 8;
+        smem = (size_t)XB + (size_t)s_ * Gm::STAGE_B + 16 * (size_t)s_ + 4 * (size_t)((s_ + 3) & ~3) + RED;
+        if (s_ >= 2)
+            cudaFuncSetAttribute(staged_mma_swiglu_kernel<CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        S = s_;
+    }
+    if (S < 2) return 1;
+    const int grid = N / 16 < num_sms() ? N / 16 : num_sms();
+    static const bool want_dbg = getenv("DS_K4_TIMELINE") != nullptr;
+    static unsigned long long* dbg = nullptr;
+    if (want_dbg && !dbg) cudaMalloc(&dbg, 8 * 1024 * sizeof(unsigned long long));
+    if (want_dbg) cudaMemsetAsync(dbg, 0, 8 * 1024 * sizeof(unsigned long long), st);
+    staged_mma_swiglu_kernel<CPL><<<grid, k4s::kThreads, smem, st>>>(x, a, b, N, S, hout, k4s_next_slot(),
+                                                                     want_dbg ? dbg : nullptr);
+    DS_LAUNCH_CHECK("ds_w4_swiglu_gemv (staged mma)");
+    if (want_dbg) {
+        static unsigned long long h[8 * 1024];
+        cudaStreamSynchronize(st);
+        cudaMemcpy(h, dbg, 8 * grid * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+        unsigned long long t0 = ~0ull, t1 = 0, t3 = 0;
+        for (int bi = 0; bi < grid; ++bi) {
+            t0 = h[8 * bi] < t0 ? h[8 * bi] : t0;
+            t3 = h[8 * bi + 3] > t3 ? h[8 * bi + 3] : t3;
+            t1 = h[8 * bi + 1] > t1 ? h[8 * bi + 1] : t1;
+        }
+        fprintf(stderr, "K4 staged mma swiglu: last first-issue %.2f us, last producer done %.2f us\n",
+                (t1 - t0) / 1e3, (t3 - t0) / 1e3);
+    }
+    return DS_OK;
+}
+
 inline bool k4_staged_enabled() {
     static const char* v = getenv("DS_K4_VARIANT");
     return !(v && (v[0] == 'v' || v[0] == 'm'));
@@ -1018,6 +1229,13 @@ template <int G>
 static int swiglu_staged(const __nv_bfloat16* x, const ds_w4_expert* e, int d, int ff, __nv_bfloat16* h,
                          cudaStream_t st) {
     if (!k4_staged_enabled() || !staged_shape_ok<G>(d, ff)) return 1;
+    static const bool mma = !(getenv("DS_K4S_MMA") && getenv("DS_K4S_MMA")[0] == '0');   // A/B runs
+    if constexpr (G == 128) {
+        if (mma && ff % 16 == 0) {
+            if (d / 1024 == 4) return staged_mma_launch<4>(x, to_ptr(e->w1), to_ptr(e->w3), ff, h, st);
+            if (d / 1024 == 6) return staged_mma_launch<6>(x, to_ptr(e->w1), to_ptr(e->w3), ff, h, st);
+        }
+    }
     static const int rb = getenv("DS_K4S_RB_UP") ? atoi(getenv("DS_K4S_RB_UP")) : 8;   // A/B runs
 #define DS_SW(CPL, RB) staged_launch<2, CPL, G, RB, true>(x, to_ptr(e->w1), to_ptr(e->w3), ff, h, nullptr, nullptr, st)
     switch (d / 1024) {

@@ -31,7 +31,7 @@ for s in $STEPS; do
       python scripts/summarize_launches.py gpurun_out/launches.csv > gpurun_out/launches_summary.md 2>&1;;
     ncu)
       log ncu
-      timeout 900 ncu --set full --clock-control none --import-source on -k regex:'swiglu_gemv|down_gemv' -s 4 -c 4 \
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:'staged_gemv|swiglu_gemv|down_gemv' -s 4 -c 4 \
         -o gpurun_out/k4 -f python scripts/kbench.py --only k4 --iters 3 > gpurun_out/ncu_k4.log 2>&1
       log "ncu k4 rc=$?"
       timeout 900 ncu --set full --clock-control none --import-source on -k regex:'w4_gemm' -s 4 -c 2 \
