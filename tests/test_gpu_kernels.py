@@ -237,3 +237,46 @@ def test_expert_gemv_and_timed_grouped_ffn_match_split_calls(cuda):
     torch.cuda.synchronize()
     assert torch.equal(hh1, hh2) and torch.equal(y1, y2)
     assert e0.elapsed_time(e1) > 0
+
+
+def test_staged_gemv_concurrent_streams_and_repeat(cuda):
+    """K4 v5 hands row blocks out through a per-launch ticket counter reset by
+    its last CTA: four expert GEMVs issued on two streams at once (they share
+    the SMs, each takes a ticket slot of its own) and 70 back-to-back launches
+    (the 64-slot counter ring wraps) give bit-identical results to one
+    expert at a time."""
+    from paper_2509_07379_b200 import ops
+    d, ff, G = 4096, 14336, 128
+    offs, total = _layout(d, ff, G)
+    E = 4
+    blobs = torch.zeros((E, total), dtype=torch.uint8, device=cuda)
+    for i in range(E):
+        _lib.call("ds_w4_generate", 21, 1, i, d, ff, G, _lib.ptr(blobs[i]), _lib.stream_ptr())
+    es = [_expert_struct(blobs[i], offs) for i in range(E)]
+    x = _rand_bf16((1, d), 1.0, torch.Generator().manual_seed(8)).to(cuda)
+    rw = torch.tensor([0.5], device=cuda)
+    ref_h, ref_a = [], []
+    for i in range(E):
+        h = torch.empty((1, ff), dtype=torch.bfloat16, device=cuda)
+        a = torch.zeros((1, d), device=cuda)
+        ops.expert_gemv(x, es[i], d, ff, G, h, rw, 1, a)
+        torch.cuda.synchronize()
+        ref_h.append(h)
+        ref_a.append(a)
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    hs = [torch.empty((1, ff), dtype=torch.bfloat16, device=cuda) for _ in range(E)]
+    acs = [torch.zeros((1, d), device=cuda) for _ in range(E)]
+    torch.cuda.synchronize()
+    for i in range(E):
+        with torch.cuda.stream(streams[i % 2]):
+            ops.expert_gemv(x, es[i], d, ff, G, hs[i], rw, 1, acs[i])
+    torch.cuda.synchronize()
+    for i in range(E):
+        assert torch.equal(hs[i], ref_h[i]) and torch.equal(acs[i], ref_a[i]), i
+    h = torch.empty((1, ff), dtype=torch.bfloat16, device=cuda)
+    for r in range(70):
+        a = torch.zeros((1, d), device=cuda)
+        ops.expert_gemv(x, es[r % E], d, ff, G, h, rw, 1, a)
+        if r % 10 == 9 or r == 69:
+            torch.cuda.synchronize()
+            assert torch.equal(h, ref_h[r % E]) and torch.equal(a, ref_a[r % E]), r
