@@ -417,7 +417,6 @@ __global__ void __launch_bounds__(k4s::kThreads, 1) staged_gemv_kernel(
     uint64_t* empty = full + S;
     int* hdr = reinterpret_cast<int*>(empty + S);         // row block of each ring slot (-1: end of stream)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int T = (N + RB - 1) / RB;                      // row blocks
     const W4Ptr W[2] = {wa, wb};
     if (threadIdx.x == 0) {
         stamp(0);
