@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--chunk-mb", type=float, default=256.0,
                     help="chunk size of confirmed transfers (re-fetches, promoted prefetches); >= the expert = whole-expert copies")
     ap.add_argument("--link-depth", type=int, default=2)
+    ap.add_argument("--pin-mb", type=float, default=0.0,
+                    help="residency-budget policy: HBM (MiB) for the most popular experts, pinned for the request")
     ap.add_argument("--spec-chunk-mb", type=float, default=0.5,
                     help="chunk size of speculative (predicted) prefetches until the gate confirms them")
     ap.add_argument("--seed", type=int, default=0)
@@ -278,7 +280,8 @@ def run_ours(args):
     eng = Engine(shape, args.policy if args.policy != "oracle" else "duoserve", seed=args.seed, device=dev,
                  store=store, predictor=net, pop=pop, aff=aff, max_seq=args.prefill + args.decode + 8,
                  max_prefill=args.prefill, cancel_mispredicted=not args.no_cancel, chunk_mb=args.chunk_mb,
-                 link_depth=args.link_depth, ep=ep, spec_chunk_mb=args.spec_chunk_mb)
+                 link_depth=args.link_depth, ep=ep, spec_chunk_mb=args.spec_chunk_mb,
+                 pin_budget_bytes=int(args.pin_mb * 2**20) if args.policy == "duoserve" else 0)
     # replicas: an independent request per rank; EP: every rank serves the same request
     gen = torch.Generator().manual_seed(args.seed + (0 if ep else 1000 * rank))
     ids_host = torch.randint(0, shape.vocab, (args.prefill,), generator=gen).pin_memory()

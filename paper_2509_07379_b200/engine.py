@@ -366,7 +366,8 @@ class Engine:
                  predictor: ExpertMLP | None = None, pop=None, aff=None, oracle_paths=None,
                  max_seq: int = 2048, max_prefill: int = 2048, cancel_mispredicted: bool = True,
                  chunk_mb: float = 256.0, link_depth: int = 2, use_graphs: bool = True,
-                 ep: EPConfig | None = None, collect_stats: bool = False, spec_chunk_mb: float = 0.5):
+                 ep: EPConfig | None = None, collect_stats: bool = False, spec_chunk_mb: float = 0.5,
+                 pin_budget_bytes: int = 0):
         self.shape = shape
         self.policy = SchedulerPolicy(policy)
         self.device = torch.device(device)
@@ -399,6 +400,12 @@ class Engine:
                 raise ValueError("policy 'oracle' needs the recorded decode routing (oracle_paths)")
             self.driver = TraceDriver(oracle_paths)
         dev = self.device
+        # residency-budget policy: the most popular experts
+        # live in HBM for the whole request within the spare residency budget
+        self.pinned = {}             # (layer, expert) -> W4Expert of an HBM-resident expert
+        self._pinned_buf = None
+        if pin_budget_bytes > 0:
+            self._pin_experts(pop, int(pin_budget_bytes))
         # decode buffers
         self.hist = torch.zeros((1, self.L * self.k), dtype=torch.int32, device=dev)
         self.idx1 = torch.empty((1, self.k), dtype=torch.int32, device=dev)
@@ -434,6 +441,32 @@ class Engine:
         self._link_peak = None
         self.last_logits = None
         self.reset()
+
+    def _pin_experts(self, pop, budget: int) -> None:
+        """Pin the (layer, expert) pairs with the highest popularity pop[l, e]
+        (ties: lower layer, then lower expert) that fit in `budget` bytes.  They
+        are copied once here, never streamed, and take no cache slot."""
+        if self.policy is SchedulerPolicy.PREFETCH_ALL:
+            raise ValueError("pinning is not defined for 'prefetchall' (every expert is streamed by design)")
+        if pop is None:
+            raise ValueError("pin_budget_bytes needs the popularity matrix (pop)")
+        vals = np.asarray(pop.values, dtype=np.float64)
+        n = min(budget // self.store.blob_bytes, self.L * len(self.owned))
+        if n <= 0:
+            return
+        cand = sorted(((l, e) for l in range(self.L) for e in self.owned), key=lambda le: (-vals[le[0], le[1]], le))
+        chosen = sorted(cand[:n])
+        self._pinned_buf = torch.empty((n, self.store.blob_bytes), dtype=torch.uint8, device=self.device)
+        for i, (l, e) in enumerate(chosen):
+            self._pinned_buf[i].copy_(self.store.blob(l, e))
+            self.pinned[(l, e)] = ops.expert_struct(self._pinned_buf[i].data_ptr(), self.d, self.ff, self.G)
+        torch.cuda.synchronize(self.device)
+
+    def _split_pinned(self, l: int, experts) -> tuple:
+        """(streamed, pinned) experts of layer l, order kept."""
+        if not self.pinned:
+            return list(experts), []
+        return [e for e in experts if (l, e) not in self.pinned], [e for e in experts if (l, e) in self.pinned]
 
     # ------------------------------------------------------------------ API
     def reset(self) -> None:
@@ -602,8 +635,12 @@ class Engine:
         if layer >= self.L or self.policy in (SchedulerPolicy.ON_DEMAND, SchedulerPolicy.PREFETCH_ALL):
             self._spec = None
             return
+        cand = [e for e in self.owned if (layer, e) not in self.pinned]
+        if not cand:                             # every expert of the layer is pinned in HBM
+            self._spec = None
+            return
         slot = self._next_ring_slot()
-        first = self.owned[0]                    # lowest (owned) expert; 0 on a single GPU
+        first = cand[0]                          # lowest (owned, streamed) expert; 0 on a single GPU
         if self.link.cancel_enabled:
             # through the native link in small chunks: if the gate leaves `first`
             # out of A_l its remaining chunks are dropped (the log is unchanged)
@@ -634,6 +671,7 @@ class Engine:
         off = self.p_off_host.tolist()
         A_all = [e for e in range(self.M) if off[e + 1] > off[e]]
         A = [e for e in A_all if e in self.owned_set]       # this rank's share (all on one GPU)
+        A, A_pin = self._split_pinned(l, A)                 # pinned experts are already in HBM
         plan = []                                           # (expert, slot, already_queued)
         if self.policy is SchedulerPolicy.PREFETCH_ALL:
             return self._moe_prefill_all(l, h, T, A, A_all, off, w, idx, idx_host)
@@ -651,7 +689,10 @@ class Engine:
                     else:
                         self.link.cancel(tr)           # wrong guess: drop its remaining chunks
             plan += [(e, self._next_ring_slot(), False) for e in A if not (spec and e == spec[2])]
-        self.log.append({"phase": "prefill", "layer": l, "fetch": [e for e, _, _ in plan], "activated": A_all})
+        self.log.append({"phase": "prefill", "layer": l, "fetch": [e for e, _, _ in plan], "activated": A_all,
+                         **({"pinned": A_pin} if self.pinned else {})})
+        for e in A_pin:
+            self._prefill_ffn(e, None, off, st=self.pinned[(l, e)])
         # sliding window over the slot ring: the copy into a slot is queued only
         # after the compute that last used it has been queued (its free event)
         window = self.n_slots if self.policy is not SchedulerPolicy.ON_DEMAND else self.n_slots
@@ -671,9 +712,10 @@ class Engine:
         self._spec_fetch(l + 1)
         return self._prefill_combine(h, T, w, idx), idx_host.numpy()
 
-    def _prefill_ffn(self, e: int, slot: int, off) -> None:
+    def _prefill_ffn(self, e: int, slot, off, st=None) -> None:
         lo, hi = off[e], off[e + 1]
-        st = self.cache.acquire(slot)
+        if st is None:
+            st = self.cache.acquire(slot)
         evs = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) if self.prof else (None, None)
         ops.grouped_ffn(self.p_xperm[lo:hi], [0, hi - lo], [st], self.d, self.ff, self.G,
                         self.p_h[lo:hi], self.p_y[lo:hi], self.p_ws, *evs)
@@ -724,6 +766,7 @@ class Engine:
         slot_of, trs = {}, {}
         miss = []
         mine = [e for e in E if e in self.owned_set]
+        mine, mine_pin = self._split_pinned(l, mine)           # pinned experts are already in HBM
         if self.policy is SchedulerPolicy.PREFETCH_ALL:
             self.log.append({"phase": "decode", "token": self.t_decode, "layer": l, "fetch": list(self.owned),
                              "kind": "prefetchall"})
@@ -738,7 +781,7 @@ class Engine:
                 trs[e] = link.submit(slot, l, e)
                 slot_of[e] = slot
             self.log.append({"phase": "decode", "token": self.t_decode, "layer": l, "fetch": mine,
-                             "kind": "ondemand"})
+                             "kind": "ondemand", **({"pinned": mine_pin} if self.pinned else {})})
         else:
             P, order, pending = self._pred_next              # pending: this rank's predicted experts
             miss = sorted(set(mine) - set(P))
@@ -758,8 +801,10 @@ class Engine:
                 slot_of[e] = s_
             self.log.append({"phase": "decode", "token": self.t_decode, "layer": l,
                              "pred": sorted(p for p in P if p in self.owned_set),
-                             "gate": sorted(E), "refetch": miss})
-        # expert compute: hits first (already resident or in flight), then re-fetched ones
+                             "gate": sorted(E), "refetch": miss, **({"pinned": mine_pin} if self.pinned else {})})
+        # expert compute: pinned, then hits (already resident or in flight), then re-fetched ones
+        for e in mine_pin:
+            self._decode_ffn(a, self.pinned[(l, e)], E.index(e))
         for e in [x for x in mine if x not in miss] + miss:
             j = E.index(e)
             link.flush(trs[e])
@@ -772,7 +817,7 @@ class Engine:
             cur = set(slot_of.values())
             free = [s_ for s_ in range(self.n_slots) if s_ not in cur][: self.k]
             pending = {}
-            for e, s_ in zip([e for e in order if e in self.owned_set], free):
+            for e, s_ in zip([e for e in order if e in self.owned_set and (l + 1, e) not in self.pinned], free):
                 pending[e] = (s_, link.submit(s_, l + 1, e, speculative=True))
             self._pred_next = (Pn, order, pending)
         return out, E
@@ -848,8 +893,11 @@ class Engine:
 
     def resident_bytes(self) -> dict:
         pred = self.driver.nbytes if isinstance(self.driver, MLPDriver) else 0
-        return {"non_moe": self.W.nbytes(), "expert_slots": self.cache.nbytes, "predictor": pred,
-                "kv_cache": self.kv.nbytes, "model_total": self.shape.total_bytes}
+        out = {"non_moe": self.W.nbytes(), "expert_slots": self.cache.nbytes, "predictor": pred,
+               "kv_cache": self.kv.nbytes, "model_total": self.shape.total_bytes}
+        if self._pinned_buf is not None:
+            out["pinned_experts"] = self._pinned_buf.numel()
+        return out
 
 
 def _union(iv: list) -> list:

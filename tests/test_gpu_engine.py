@@ -168,3 +168,43 @@ def test_online_routing_stats_equal_reference_counting(tiny, cuda):
     dp, da = S.count_on_device(big, cuda)
     assert np.array_equal(dp.counts, S.build_popularity(big).counts)
     assert np.array_equal(da.values, S.build_affinity(big).values)
+
+
+def test_pinned_experts_same_tokens_never_streamed(tiny, cuda):
+    """Residency-budget policy: the 3 most popular
+    (layer, expert) pairs live in HBM.  Pinning changes data movement only:
+    same tokens and routing, predictions and gate sets unchanged, pinned experts
+    never in a fetch / refetch list, exactly their transfers saved."""
+    shape = tiny["shape"]
+    base = tiny["eng"]
+    blob = base.store.blob_bytes
+    kw = dict(seed=3, dense=tiny["dense"].to(cuda), predictor=tiny["net"], pop=tiny["pop"], aff=tiny["aff"],
+              max_seq=PREFILL + DECODE + 8, max_prefill=PREFILL)
+    ref = Engine(shape, "duoserve", **kw)
+    assert ref.generate(tiny["ids"], DECODE) == tiny["toks"]
+    eng = Engine(shape, "duoserve", pin_budget_bytes=3 * blob + blob // 2, **kw)
+    vals = tiny["pop"].values
+    want = sorted(((l, e) for l in range(shape.num_layers) for e in range(8)), key=lambda le: (-vals[le], le))[:3]
+    assert sorted(eng.pinned) == sorted(want)
+    assert eng.resident_bytes()["pinned_experts"] == 3 * blob
+    assert eng.generate(tiny["ids"], DECODE) == tiny["toks"]
+    assert eng.paths_decode == ref.paths_decode
+    assert len(eng.log) == len(ref.log)
+    saved = 0
+    for r0, r in zip(ref.log, eng.log):
+        l = r["layer"]
+        pins = {e for (ll, e) in eng.pinned if ll == l}
+        assert (r["phase"], l) == (r0["phase"], r0["layer"])
+        if r["phase"] == "prefill":
+            assert r["activated"] == r0["activated"]
+            assert set(r["fetch"]) == set(r0["fetch"]) - pins
+            assert set(r["pinned"]) == set(r0["activated"]) & pins
+        elif "refetch" in r0:
+            assert r["pred"] == r0["pred"] and r["gate"] == r0["gate"]
+            assert r["refetch"] == [e for e in r0["refetch"] if e not in pins]
+            assert set(r["pinned"]) == set(r0["gate"]) & pins
+        else:
+            assert r["fetch"] == [e for e in r0["fetch"] if e not in pins]
+        saved += len(r["pinned"])
+    assert saved > 0
+    assert eng.h2d_bytes() < ref.h2d_bytes()
