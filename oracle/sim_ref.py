@@ -36,35 +36,44 @@ def _sorted(x):
     return [int(e) for e in sorted(x)]
 
 
-def cache_log_prefill(E_by_token, L: int, policy: str = "duoserve", owned=None, M: int = 8):
+def cache_log_prefill(E_by_token, L: int, policy: str = "duoserve", owned=None, M: int = 8, pinned=None):
     """E_by_token: list over prefill tokens of L-tuples of selections.
     owned: expert ids of this rank under expert parallelism (None = all);
     the speculative first transfer is then the rank's lowest owned expert.
-    M: experts per layer (used by prefetchall only)."""
+    M: experts per layer (used by prefetchall only).
+    pinned: (layer, expert) pairs resident in HBM for the whole request
+    (residency-budget extension): never fetched, no
+    speculative transfer, listed under "pinned" when activated."""
     log = []
     for l in range(L):
         A = set()
         for path in E_by_token:
             A.update(path[l])
         mine = A if owned is None else A & set(owned)
-        first = 0 if owned is None else min(owned)
+        pins = {e for (ll, e) in (pinned or ()) if ll == l}
+        cand = [e for e in (range(M) if owned is None else sorted(owned)) if e not in pins]
+        first = cand[0] if cand else None
         if policy in ("duoserve", "oracle"):
-            fetch = [first] + _sorted(mine - {first})
+            fetch = ([first] if first is not None else []) + _sorted(mine - pins - {first})
         elif policy == "ondemand":
-            fetch = _sorted(mine)
+            fetch = _sorted(mine - pins)
         elif policy == "prefetchall":
             fetch = list(range(M)) if owned is None else _sorted(owned)
         else:
             raise ValueError(policy)
         log.append({"phase": "prefill", "layer": l, "fetch": fetch, "activated": _sorted(A)})
+        if pinned:
+            log[-1]["pinned"] = _sorted(mine & pins)
     return log
 
 
-def cache_log_decode(paths, preds, L: int, policy: str = "duoserve", owned=None, M: int = 8):
+def cache_log_decode(paths, preds, L: int, policy: str = "duoserve", owned=None, M: int = 8, pinned=None):
     """paths[t][l] = gate selection of decode token t at layer l;
     preds[t][l] = predicted set for l >= 1 (ignored for ondemand/prefetchall).
     owned: expert ids of this rank under expert parallelism (None = all).
-    M: experts per layer (used by prefetchall only)."""
+    M: experts per layer (used by prefetchall only).
+    pinned: (layer, expert) pairs resident in HBM (see cache_log_prefill): never
+    fetched or re-fetched, not counted as prefetch hits / misses."""
     own = None if owned is None else set(owned)
     keep = (lambda xs: _sorted(xs)) if own is None else (lambda xs: _sorted(set(xs) & own))
     log = []
@@ -72,19 +81,23 @@ def cache_log_decode(paths, preds, L: int, policy: str = "duoserve", owned=None,
     for t, path in enumerate(paths):
         for l in range(L):
             E = _sorted(path[l])
+            pins = {e for (ll, e) in (pinned or ()) if ll == l}
+            extra = {"pinned": _sorted(set(keep(E)) & pins)} if pinned else {}
             if policy == "prefetchall":
                 log.append({"phase": "decode", "token": t, "layer": l,
                             "fetch": list(range(M)) if own is None else _sorted(own), "kind": "prefetchall"})
                 continue
             if l == 0 or policy == "ondemand":
-                log.append({"phase": "decode", "token": t, "layer": l, "fetch": keep(E), "kind": "ondemand"})
+                log.append({"phase": "decode", "token": t, "layer": l,
+                            "fetch": [e for e in keep(E) if e not in pins], "kind": "ondemand", **extra})
                 continue
             P = keep(preds[t][l])
-            miss = _sorted(set(keep(E)) - set(P))
-            hits += len(set(keep(E)) & set(P))
+            Ed = set(keep(E)) - pins
+            miss = _sorted(Ed - set(P))
+            hits += len(Ed & set(P))
             misses += len(miss)
             refetches += len(miss)
-            log.append({"phase": "decode", "token": t, "layer": l, "pred": P, "gate": E, "refetch": miss})
+            log.append({"phase": "decode", "token": t, "layer": l, "pred": P, "gate": E, "refetch": miss, **extra})
     return log, {"prefetch_hits": hits, "prefetch_misses": misses, "refetch_count": refetches}
 
 

@@ -781,7 +781,7 @@ class Engine:
                 trs[e] = link.submit(slot, l, e)
                 slot_of[e] = slot
             self.log.append({"phase": "decode", "token": self.t_decode, "layer": l, "fetch": mine,
-                             "kind": "ondemand", **({"pinned": mine_pin} if self.pinned else {})})
+                             "kind": "ondemand", **({"pinned": sorted(mine_pin)} if self.pinned else {})})
         else:
             P, order, pending = self._pred_next              # pending: this rank's predicted experts
             miss = sorted(set(mine) - set(P))
@@ -801,7 +801,7 @@ class Engine:
                 slot_of[e] = s_
             self.log.append({"phase": "decode", "token": self.t_decode, "layer": l,
                              "pred": sorted(p for p in P if p in self.owned_set),
-                             "gate": sorted(E), "refetch": miss, **({"pinned": mine_pin} if self.pinned else {})})
+                             "gate": sorted(E), "refetch": miss, **({"pinned": sorted(mine_pin)} if self.pinned else {})})
         # expert compute: pinned, then hits (already resident or in flight), then re-fetched ones
         for e in mine_pin:
             self._decode_ffn(a, self.pinned[(l, e)], E.index(e))

@@ -208,3 +208,15 @@ def test_pinned_experts_same_tokens_never_streamed(tiny, cuda):
         saved += len(r["pinned"])
     assert saved > 0
     assert eng.h2d_bytes() < ref.h2d_bytes()
+    # and the log equals the simulator oracle's with the same pinned set
+    L = shape.num_layers
+    pre_paths = [tuple(tuple(int(e) for e in eng.paths_prefill[t, l]) for l in range(L)) for t in range(PREFILL)]
+    ref_net = predictor_ref.RefNet(tiny["net"].input_dim, 8, tiny["net"].hidden, 0)
+    preds = []
+    for path in eng.paths_decode:
+        sets, _ = predictor_ref.predict_sets(ref_net, [path] * (L - 1), list(range(1, L)), tiny["pop"].values,
+                                             tiny["aff"].values, 2)
+        preds.append([None] + [tuple(x) for x in sets])
+    pins = set(eng.pinned)
+    assert eng.log[:L] == sim_ref.cache_log_prefill(pre_paths, L, "duoserve", pinned=pins)
+    assert eng.log[L:] == sim_ref.cache_log_decode(eng.paths_decode, preds, L, "duoserve", pinned=pins)[0]

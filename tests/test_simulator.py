@@ -250,3 +250,34 @@ def test_b200_calibrated_preset():
     per_tok = (m.e2e_s - m.ttft_s) / m.decode_tokens
     floor = L * cfg.top_k * cost.transfer_time_s(cfg.expert_bytes)
     assert floor <= per_tok < 1.2 * floor
+
+
+def test_oracle_pinned_extension_properties():
+    """sim_ref's residency-budget extension: an empty pin
+    set changes nothing; pinned experts never appear in a fetch / refetch
+    list and are reported under "pinned" when the gate or prefill uses them;
+    the speculative prefill transfer skips a pinned expert 0."""
+    rng = np.random.default_rng(3)
+    L, M, k = 4, 8, 2
+    pre = [tuple(tuple(int(e) for e in rng.choice(M, k, replace=False)) for _ in range(L)) for _ in range(16)]
+    paths = [tuple(tuple(int(e) for e in rng.choice(M, k, replace=False)) for _ in range(L)) for _ in range(6)]
+    preds = [[None] + [tuple(int(e) for e in rng.choice(M, k, replace=False)) for _ in range(1, L)] for _ in paths]
+    for pol in ("duoserve", "ondemand"):
+        assert sim_ref.cache_log_prefill(pre, L, pol, pinned=set()) == sim_ref.cache_log_prefill(pre, L, pol)
+        assert sim_ref.cache_log_decode(paths, preds, L, pol, pinned=set()) == \
+            sim_ref.cache_log_decode(paths, preds, L, pol)
+    pins = {(0, 0), (1, 3), (2, 5), (3, 1)}
+    lp = sim_ref.cache_log_prefill(pre, L, "duoserve", pinned=pins)
+    for r in lp:
+        pl = {e for (ll, e) in pins if ll == r["layer"]}
+        assert not pl & set(r["fetch"])
+        assert set(r["pinned"]) == set(r["activated"]) & pl
+    assert lp[0]["fetch"][0] == 1                         # expert 0 pinned at layer 0: speculate on 1
+    ld, cnt = sim_ref.cache_log_decode(paths, preds, L, "duoserve", pinned=pins)
+    _, cnt0 = sim_ref.cache_log_decode(paths, preds, L, "duoserve")
+    n_pin = 0
+    for r in ld:
+        pl = {e for (ll, e) in pins if ll == r["layer"]}
+        assert not pl & set(r.get("refetch", r.get("fetch", [])))
+        n_pin += len(r["pinned"]) if r["layer"] > 0 else 0
+    assert cnt["prefetch_hits"] + cnt["prefetch_misses"] + n_pin == cnt0["prefetch_hits"] + cnt0["prefetch_misses"]
