@@ -957,15 +957,15 @@ inline unsigned k4s_next_slot() {
 }
 
 // v5 SwiGLU GEMV with the tensor cores (G = 128, R = 1): the same producer /
-// ring / ticket structure with 16-row blocks; the 16 consumer warps form two
-// groups of 8, a group takes a block and splits K: warp w of the group owns
-// quantisation groups [w*GPR/8, (w+1)*GPR/8) of all 16 rows.  Per group,
+// ring / ticket structure with 16-row blocks; the 16 consumer warps take a
+// block together and split K: warp w owns quantisation groups
+// [w*GPR/16, (w+1)*GPR/16) of all 16 rows.  Per group,
 // lane (g, t) dequantises code chunk t of rows g and g+8 straight into
 // mma.m16n8k16 A fragments (v3's mapping: 8 mmas per matrix per group, the k
 // permutation inside an mma applied to x as well), x (unswizzled in shared
 // memory) gives the B fragments, and the group scale is factored out with a
 // precomputed per-group sum of x:  s * (D - (128 + z) * sum_group x).  With
-// one activation row every D column holds the same dot product.  The 8
+// one activation row every D column holds the same dot product.  The 16
 // partial sums per row are reduced through shared memory in a fixed order
 // (deterministic); 2.3x fewer issue slots per weight than the FHFMA
 // consumer, which is issue-bound on the SwiGLU half.
@@ -977,7 +977,7 @@ __global__ void __launch_bounds__(k4s::kThreads, 1) staged_mma_swiglu_kernel(
     constexpr int NMAT = 2, G = 128, RB = 16;
     using Gm = k4s::Geo<NMAT, CPL, G, RB>;
     constexpr int K = Gm::K, GPR = Gm::GPR;
-    constexpr int WPG = 8;                                  // warps per block (K split)
+    constexpr int WPG = k4s::kConsumers;                    // warps per block (K split): one group
     constexpr int NG = k4s::kConsumers / WPG;               // consumer groups
     constexpr int GPW = GPR / WPG;                          // quantisation groups per warp
     constexpr int XB = (K * 2 + GPR * 4 + 127) & ~127;
@@ -1116,7 +1116,7 @@ template <int CPL>
 static int staged_mma_launch(const __nv_bfloat16* x, W4Ptr a, W4Ptr b, int N, __nv_bfloat16* hout, cudaStream_t st) {
     using Gm = k4s::Geo<2, CPL, 128, 16>;
     constexpr int XB = (Gm::K * 2 + Gm::GPR * 4 + 127) & ~127;
-    constexpr int RED = 2 * 2 * 8 * 2 * 16 * 4;
+    constexpr int RED = 2 * 1 * 16 * 2 * 16 * 4;            // [parity][NG = 1][WPG = 16][NMAT][16 rows]
     static int S = -1;
     static size_t smem = 0;
     if (S < 0) {
@@ -1166,6 +1166,11 @@ static int staged_launch(const __nv_bfloat16* x, W4Ptr a, W4Ptr b, int N, __nv_b
     if (S < 0) {
         int s_ = (k4s::kSmemBudget - Gm::X_B) / (Gm::STAGE_B + 20);
         if (s_ > 8) s_ = 8;
+        // ring depth a multiple of the consumer-group count: slot j then always
+        // serves the same group, so a group never waits on a slot whose previous
+        // phase (another group's stage, possibly still landing) is incomplete —
+        // with mbarrier parity waits that phase would alias the awaited one
+        s_ -= s_ % (k4s::kConsumers / RB);
         smem = (size_t)Gm::X_B + (size_t)s_ * Gm::STAGE_B + 20 * (size_t)s_;
         if (s_ >= 2)
             cudaFuncSetAttribute(staged_gemv_kernel<NMAT, CPL, G, RB, SWIGLU>,
