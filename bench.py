@@ -267,7 +267,7 @@ def run_ours(args):
     from paper_2509_07379_b200.engine import Engine
     shape = load_shape(args.config)
     t_setup = time.time()
-    net, pop, aff = predictor_inputs(shape) if args.policy == "duoserve" else (None, None, None)
+    net, pop, aff = predictor_inputs(shape) if args.policy in ("duoserve", "oracle") else (None, None, None)
     ep = None
     if args.ep and ws > 1:
         from paper_2509_07379_b200.ep import EPConfig
