@@ -261,38 +261,50 @@ def run_ours(args):
     rank, ws, lr = dist_init()
     dev = torch.device("cuda", lr)
     torch.cuda.set_device(dev)
+    from paper_2509_07379_b200 import numa
+    numa_info = numa.bind_to_gpu_node(lr)    # pinned store + link threads on the GPU's own socket
     from paper_2509_07379_b200 import _lib
     _lib.load()                          # fail loudly if the CUDA library is missing
     from paper_2509_07379_b200.config import load_shape
     from paper_2509_07379_b200.engine import Engine
     shape = load_shape(args.config)
     t_setup = time.time()
-    net, pop, aff = predictor_inputs(shape) if args.policy in ("duoserve", "oracle") else (None, None, None)
+    if args.pin_mb > 0 and args.policy == "prefetchall":
+        raise SystemExit("--pin-mb does not apply to --policy prefetchall (every expert is streamed by design)")
+    wd = args.warmup_decode if args.warmup_decode is not None else args.decode
+    net, pop, aff = predictor_inputs(shape) if args.policy in ("duoserve", "oracle") or args.pin_mb > 0 \
+        else (None, None, None)
+    # replicas: an independent request per rank; EP: every rank serves the same request
+    gen = torch.Generator().manual_seed(args.seed + (0 if args.ep else 1000 * rank))
+    ids_host = torch.randint(0, shape.vocab, (args.prefill,), generator=gen).pin_memory()
     ep = None
     if args.ep and ws > 1:
         from paper_2509_07379_b200.ep import EPConfig
         ep = EPConfig(rank, ws, combine=args.ep_combine)
     store = None
     if ws > 1 and ep is None:
-        # replicas of one model: one shared pinned copy of the expert store per node
+        # replicas of one model: one shared pinned copy of the expert store per
+        # (host, PID namespace, NUMA node) — i.e. one per socket
         from paper_2509_07379_b200.engine import HostExpertStore
-        store = HostExpertStore(shape, args.seed, dev, shared_group=dist.group.WORLD)
-    eng = Engine(shape, args.policy if args.policy != "oracle" else "duoserve", seed=args.seed, device=dev,
-                 store=store, predictor=net, pop=pop, aff=aff, max_seq=args.prefill + args.decode + 8,
-                 max_prefill=args.prefill, cancel_mispredicted=not args.no_cancel, chunk_mb=args.chunk_mb,
-                 link_depth=args.link_depth, ep=ep, spec_chunk_mb=args.spec_chunk_mb,
-                 pin_budget_bytes=int(args.pin_mb * 2**20) if args.policy == "duoserve" else 0)
-    # replicas: an independent request per rank; EP: every rank serves the same request
-    gen = torch.Generator().manual_seed(args.seed + (0 if ep else 1000 * rank))
-    ids_host = torch.randint(0, shape.vocab, (args.prefill,), generator=gen).pin_memory()
+        grp, members = numa.store_sharing_group(numa_info["node"])
+        if len(members) > 1:
+            store = HostExpertStore(shape, args.seed, dev, shared_group=grp)
+    n_record = max(args.decode, wd)
+    serve_kw = dict(seed=args.seed, device=dev, ep=ep, max_seq=args.prefill + n_record + 8,
+                    max_prefill=args.prefill, cancel_mispredicted=not args.no_cancel, chunk_mb=args.chunk_mb,
+                    link_depth=args.link_depth, spec_chunk_mb=args.spec_chunk_mb,
+                    pin_budget_bytes=int(args.pin_mb * 2**20))
     if args.policy == "oracle":
-        # record the routing once, then replay it as the perfect predictor (SPEC DuoServeOracle)
-        eng.reset()
-        eng.generate(ids_host, args.decode + 1)
-        paths = eng.paths_decode
-        eng = Engine(shape, "oracle", seed=args.seed, device=dev, dense=eng.W, store=eng.store,
-                     oracle_paths=paths, ep=ep, max_seq=args.prefill + args.decode + 8, max_prefill=args.prefill,
-                     cancel_mispredicted=not args.no_cancel, chunk_mb=args.chunk_mb, link_depth=args.link_depth)
+        # record the routing once with the predictor-driven engine, then replay
+        # it as the perfect predictor (SPEC DuoServeOracle) on the same weights
+        rec = Engine(shape, "duoserve", store=store, predictor=net, pop=pop, aff=aff, **serve_kw)
+        rec.reset()
+        rec.generate(ids_host, n_record + 1)
+        eng = Engine(shape, "oracle", dense=rec.W, store=rec.store, oracle_paths=rec.paths_decode, pop=pop,
+                     **serve_kw)
+        del rec
+    else:
+        eng = Engine(shape, args.policy, store=store, predictor=net, pop=pop, aff=aff, **serve_kw)
     setup_s = time.time() - t_setup
     prof = eng.enable_profile()
     eng.link_peak_gbs()
@@ -320,7 +332,6 @@ def run_ours(args):
                 "h2d_experts": eng.h2d_bytes() - c0, "tokens": toks,
                 "d2h": eng.d2h_bytes}
 
-    wd = args.warmup_decode if args.warmup_decode is not None else args.decode
     for _ in range(args.warmup):
         one_step(wd)
     prof.reset()
@@ -381,7 +392,7 @@ def run_ours(args):
                                f"{'' if args.no_cancel else ' + chunked cancellable prefetch'}",
                    "model": shape.name, "global_batch": 1 if ep else ws, "seq_len": args.prefill + args.decode,
                    "parallelism": (f"ep{ws}-{ep.combine}" if ep else f"replicas{ws}") if ws > 1 else "single-gpu",
-                   "expert_slots": eng.n_slots,
+                   "expert_slots": eng.n_slots, "numa": numa_info,
                    "l2": "inputs > L2: every expert byte is streamed from pinned host memory per request"},
         "ttft_ms": round(ttft, 2), "decode_tok_s": round(args.decode / (dec_ms / 1e3), 3),
         "decode_ms_per_token": round(dec_ms / args.decode, 3),

@@ -72,11 +72,16 @@ class HostExpertStore:
         shape3 = (L, len(self.experts), self.blob_bytes)
         fill = True
         self._registered = None
+        self.data = None
         if shared_group is not None:
             self.data, fill = _shared_pinned(shape3, shared_group)
-            self._registered = self.data
-        else:
+            if self.data is None:                     # ranks cannot share: private store each
+                shared_group, fill = None, True
+            else:
+                self._registered = self.data
+        if self.data is None:
             self.data = torch.empty(shape3, dtype=torch.uint8, pin_memory=True)
+        self.shared = shared_group is not None
         self.alloc_s = time.time() - t0
         if not fill:                                  # another rank generates the bytes
             import torch.distributed as dist
@@ -101,16 +106,35 @@ class HostExpertStore:
     def blob(self, layer: int, expert: int) -> torch.Tensor:
         return self.data[layer, self.local[expert]]
 
+    def close(self) -> None:
+        """Unpin a shared (cudaHostRegister'd) mapping; private stores are
+        cudaHostAlloc memory freed with the tensor."""
+        if self._registered is not None:
+            _unregister(self._registered)
+            self._registered = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
     @property
     def nbytes(self) -> int:
         return self.data.numel()
 
 
 def _shared_pinned(shape3: tuple, group) -> tuple:
-    """(u8 host tensor of shape3 shared by all ranks of `group`, is_creator).
-    Rank 0 of the group creates an anonymous memfd, the others map it through
-    /proc/<pid>/fd; every rank pins its mapping with cudaHostRegister (a
-    registered mapping is DMA-able like cudaHostAlloc memory)."""
+    """(u8 host tensor of shape3 shared by all ranks of `group`, is_creator),
+    or (None, False) on every rank when the ranks cannot share.
+
+    `group` must hold ranks of one host and one PID namespace (see
+    numa.store_sharing_group): rank 0 of the group creates an anonymous memfd,
+    the others map it through /proc/<pid>/fd.  If any rank fails to open the
+    path (another host or PID namespace) every rank falls back to a private
+    store.  Every rank pins its mapping with cudaHostRegister (a registered
+    mapping is DMA-able like cudaHostAlloc memory); release it with
+    _unregister."""
     import os
     import torch.distributed as dist
     nbytes = 1
@@ -124,15 +148,27 @@ def _shared_pinned(shape3: tuple, group) -> tuple:
         os.ftruncate(fd, nbytes)
         path[0] = f"/proc/{os.getpid()}/fd/{fd}"
     dist.broadcast_object_list(path, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
-    flat = torch.from_file(path[0], shared=True, size=nbytes, dtype=torch.uint8)
-    dist.barrier(group=group)                      # every rank holds a mapping
+    flat, ok = None, 1
+    try:
+        flat = torch.from_file(path[0], shared=True, size=nbytes, dtype=torch.uint8)
+    except (RuntimeError, OSError):
+        ok = 0
+    okt = torch.tensor([ok], dtype=torch.int64)
+    dist.all_reduce(okt, op=dist.ReduceOp.MIN, group=group)       # every rank holds a mapping?
     if fd is not None:
         os.close(fd)
+    if int(okt) == 0:
+        return None, False
     if torch.cuda.is_available():
         rc = torch.cuda.cudart().cudaHostRegister(flat.data_ptr(), nbytes, 0)
         if int(rc) != 0:
             raise RuntimeError(f"cudaHostRegister of the shared expert store failed ({rc})")
     return flat.view(shape3), rank == 0
+
+
+def _unregister(t: torch.Tensor) -> None:
+    if t is not None and torch.cuda.is_available():
+        torch.cuda.cudart().cudaHostUnregister(t.data_ptr())
 
 
 class ExpertCache:
@@ -388,6 +424,7 @@ class Engine:
         self.link = LinkQueue(self.cache, int(chunk_mb * 2**20) if cancel_mispredicted else 0,
                               link_depth if cancel_mispredicted else 2, cancel_mispredicted,
                               spec_chunk_bytes=int(spec_chunk_mb * 2**20))
+        self.max_seq, self.max_prefill = int(max_seq), int(max_prefill)
         self.kv = KVCache(sh, max_seq, self.device)
         self.cos, self.sin = rope_tables(sh, max_seq, self.device)
         self.driver = None
@@ -499,6 +536,12 @@ class Engine:
         """Prompt pass; returns the first generated token (greedy)."""
         ids = torch.as_tensor(ids, dtype=torch.long, device=self.device).reshape(-1)
         T = ids.numel()
+        if T < 1:
+            raise ValueError("prefill needs at least one prompt token")
+        if T > self.max_prefill:
+            raise ValueError(f"prompt of {T} tokens exceeds max_prefill={self.max_prefill}")
+        if T > self.max_seq:
+            raise ValueError(f"prompt of {T} tokens exceeds max_seq={self.max_seq}")
         h = self.W.embed[ids]
         idx_all = []
         if self.policy is SchedulerPolicy.PREFETCH_ALL:
@@ -523,7 +566,11 @@ class Engine:
     @torch.no_grad()
     def decode_step(self) -> int:
         """One greedy decode token (feeds back the previous output token)."""
+        if self.token is None:
+            raise ValueError("decode_step before prefill")
         pos = self.kv.len
+        if pos + 1 > self.max_seq:
+            raise ValueError(f"decode position {pos} would exceed max_seq={self.max_seq}")
         if self.use_graphs:
             self._ensure_decode_graphs()
             self.g_pos.fill_(pos)
@@ -879,16 +926,25 @@ class Engine:
         return self.L * self.k * self.store.blob_bytes
 
     def hit_summary(self) -> dict:
+        """Prediction counters over the decode log, counted like
+        oracle/sim_ref.cache_log_decode: prediction and gate sets restricted to
+        this rank's streamed experts (owned, not pinned), so a pinned expert is
+        never a prefetch hit and under EP a rank scores only its own experts."""
         dec = [r for r in self.log if r["phase"] == "decode" and "pred" in r]
-        hits = sum(len(set(r["pred"]) & set(r["gate"])) for r in dec)
+
+        def streamed(r, key):
+            pins = {e for (ll, e) in self.pinned if ll == r["layer"]}
+            return {e for e in r[key] if e in self.owned_set and e not in pins}
+
+        hits = sum(len(streamed(r, "pred") & streamed(r, "gate")) for r in dec)
         miss = sum(len(r["refetch"]) for r in dec)
-        exact = sum(r["pred"] == r["gate"] for r in dec)
+        exact = sum(streamed(r, "pred") == streamed(r, "gate") for r in dec)
         n = len(dec)
         return {"policy": self.policy.value, "cancel_mispredicted": self.cancel_mispredicted,
                 "chunk_bytes": self.link.chunk, "spec_chunk_bytes": self.link.spec_chunk, **self.link.stats(),
                 "prefetch_hits": hits, "prefetch_misses": miss,
                 "topk_hit_rate": round(exact / n, 4) if n else None,
-                "at_least_one_rate": round(sum(bool(set(r["pred"]) & set(r["gate"])) for r in dec) / n, 4)
+                "at_least_one_rate": round(sum(bool(streamed(r, "pred") & streamed(r, "gate")) for r in dec) / n, 4)
                 if n else None}
 
     def resident_bytes(self) -> dict:

@@ -52,6 +52,10 @@ def gate_topk(x: torch.Tensor, wg: torch.Tensor, k: int, idx: torch.Tensor, w: t
               logits: torch.Tensor | None = None) -> None:
     T, d = x.shape
     M = wg.shape[0]
+    if idx.shape[0] < T or w.shape[0] < T or idx.shape[-1] < k or w.shape[-1] < k:
+        raise ValueError(f"gate_topk: idx {tuple(idx.shape)} / w {tuple(w.shape)} too small for {T} tokens x top-{k}")
+    if hist is not None and hist.shape[0] < T:
+        raise ValueError(f"gate_topk: hist has {hist.shape[0]} rows for {T} tokens")
     stride = hist.shape[-1] if hist is not None else 0
     _lib.call("ds_gate_topk", ptr(x), ptr(wg), T, d, M, k, ptr(idx), ptr(w), ptr(logits), ptr(counts),
               ptr(hist), stride, layer, stream_ptr())
@@ -60,6 +64,8 @@ def gate_topk(x: torch.Tensor, wg: torch.Tensor, k: int, idx: torch.Tensor, w: t
 
 def permute(idx: torch.Tensor, x: torch.Tensor, M: int, offsets, pos, src, xperm) -> None:
     T, k = idx.shape
+    if x.shape[0] < T or pos.numel() < T * k or src.numel() < T * k or (xperm is not None and xperm.shape[0] < T * k):
+        raise ValueError(f"permute: buffers too small for {T} tokens x top-{k}")
     _lib.call("ds_permute", ptr(idx), ptr(x), T, x.shape[1], M, k, ptr(offsets), ptr(pos), ptr(src),
               ptr(xperm), stream_ptr())
     _count("ds_permute", 2 if xperm is not None else 1)

@@ -72,6 +72,7 @@ class EventTimeline:
 
     def __init__(self):
         self.events: list[Event] = []
+        self.cache_log: list = []         # filled by simulate_request (B200 addition)
 
     def add(self, stream: str, kind: str, start: int, end: int, **payload) -> Event:
         if stream not in _PRIO:
@@ -464,7 +465,7 @@ def _requests(traces) -> list:
 
 def simulate_request(policy, traces, cfg: ModelConfig, cost: CostModel, net=None, pop=None, aff=None,
                      seed: int = 0, check: bool = True, prefill_non_moe_s: float | None = None,
-                     cancel_chunk_bytes: int | None = None):
+                     cancel_chunk_bytes: int | None = None, return_log: bool = False):
     """Simulate one request (its prefill + decode traces) under a policy.
 
     net: a predictor object with ``predict(trace, l) -> tuple`` (the
@@ -474,7 +475,9 @@ def simulate_request(policy, traces, cfg: ModelConfig, cost: CostModel, net=None
     calibration; default: cost.non_moe_compute_per_layer_s as in the SPEC).
     cancel_chunk_bytes: model the B200 runtime's cancellable chunked prefetch
     (a wrong prefetch stops one chunk after the gate); None = SPEC semantics.
-    Returns (RequestMetrics, EventTimeline, cache log)."""
+    Returns (RequestMetrics, EventTimeline) as SPEC.md:365 specifies; with
+    return_log=True also the cache log (a third element), which the timeline
+    carries as ``EventTimeline.cache_log`` in either case."""
     pol = SchedulerPolicy(policy)
     traces = list(traces)
     reqs = _requests(traces)
@@ -523,7 +526,10 @@ def simulate_request(policy, traces, cfg: ModelConfig, cost: CostModel, net=None
                        peak_mem_bytes=compute_peak_memory(pol, cfg), prefetch_hits=st.hits,
                        prefetch_misses=st.misses, refetch_count=st.refetches, link_busy_s=st.link_busy / 1e9,
                        link_bytes=st.link_bytes)
-    return m, st.tl, st.log
+    st.tl.cache_log = st.log
+    if return_log:
+        return m, st.tl, st.log
+    return m, st.tl
 
 
 def config_digest(cfg: ModelConfig, cost: CostModel) -> str:
@@ -540,7 +546,7 @@ def run_experiment(policies, dataset: TraceDataset, cfg: ModelConfig, cost: Cost
         pol = SchedulerPolicy(p)
         rep = SimReport(policy=pol.value, seed=seed, config_digest=config_digest(cfg, cost))
         for rid, pre, dec in _requests(dataset.traces):
-            m, _, _ = simulate_request(pol, pre + dec, cfg, cost, net=net, seed=seed)
+            m, _ = simulate_request(pol, pre + dec, cfg, cost, net=net, seed=seed)
             rep.requests.append(m)
         reports[pol.value] = rep
     return reports

@@ -201,7 +201,8 @@ cancel = eng.link.depth * eng.link.spec_chunk
 for pol in ("duoserve", "duoserve+cancel", "oracle", "ondemand", "prefetchall"):
     mm, _, log = S.simulate_request(pol.split("+")[0], traces, cfg, cost, net=pp,
                                     prefill_non_moe_s=res["prefill_non_moe_s"],
-                                    cancel_chunk_bytes=cancel if pol.endswith("+cancel") else None)
+                                    cancel_chunk_bytes=cancel if pol.endswith("+cancel") else None,
+                                    return_log=True)
     sim[pol] = {"ttft_ms": mm.ttft_s * 1e3, "decode_ms_per_token": (mm.e2e_s - mm.ttft_s) * 1e3 / a.decode,
                 "refetch_count": mm.refetch_count, "link_bytes": mm.link_bytes}
     if pol.startswith("duoserve"):

@@ -52,7 +52,7 @@ def test_prefill_fixtures(policy, Tm, Cm, expect):
     cost = _cost(Tm, Cm, nm_ms=10)
     reqs = _req([((0, 1),), ((2, 3),)], [((0, 1),)])
     net = OraclePredictor()
-    _, tl, log = S.simulate_request(policy, reqs, cfg, cost, net=net)
+    _, tl, log = S.simulate_request(policy, reqs, cfg, cost, net=net, return_log=True)
     assert _moe_block(tl, 0) == expect * MS
     assert log[0]["fetch"] == [0, 1, 2, 3]
 
@@ -88,15 +88,15 @@ def test_decode_fixtures():
     cost = _cost(10, 2, nm_ms=1)
     path = tuple((2 * (l % 4), 2 * (l % 4) + 1) for l in range(L))
     reqs = _req([path], [path])
-    m, tl, log = S.simulate_request("duoserve", reqs, cfg, cost, net=OraclePredictor())
+    m, tl, log = S.simulate_request("duoserve", reqs, cfg, cost, net=OraclePredictor(), return_log=True)
     d = _decode_layer_durations(tl, 1)
     assert d[2:] == [20 * MS] * (L - 3)
     assert m.prefetch_hits == 2 * (L - 1) and m.prefetch_misses == 0
-    m, tl, log = S.simulate_request("duoserve", reqs, cfg, cost, net=_OneMissAt(4))
+    m, tl, log = S.simulate_request("duoserve", reqs, cfg, cost, net=_OneMissAt(4), return_log=True)
     d = _decode_layer_durations(tl, 1)
     assert d[3] == 30 * MS and d[4] == 20 * MS and d[5] == 20 * MS   # layers 3->4 carries the re-fetch
     assert m.refetch_count == 1 and m.prefetch_misses == 1 and m.prefetch_hits == 2 * (L - 1) - 1
-    m, tl, log = S.simulate_request("ondemand", reqs, cfg, cost)
+    m, tl, log = S.simulate_request("ondemand", reqs, cfg, cost, return_log=True)
     assert _decode_layer_durations(tl, 1) == [25 * MS] * (L - 1)
 
 
@@ -116,7 +116,7 @@ def test_cache_log_equals_oracle():
         pre = [t for t in trs if t.phase == "prefill"]
         dec = sorted([t for t in trs if t.phase == "decode"], key=lambda t: t.token_index)
         for pol in ("duoserve", "oracle", "ondemand", "prefetchall"):
-            _, _, log = S.simulate_request(pol, trs, cfg, cost, net=pp)
+            _, _, log = S.simulate_request(pol, trs, cfg, cost, net=pp, return_log=True)
             exp = sim_ref.cache_log_prefill([t.path for t in pre], L, pol)
             preds = [[None] + [pp.predict(t, l) if pol == "duoserve" else t.path[l] for l in range(1, L)]
                      for t in dec]
@@ -133,7 +133,7 @@ def test_invariants_and_metrics():
     pp = PopularityPredictor(ST.build_popularity(ds), cfg.top_k)
     for rid, trs in ds.by_request().items():
         for pol in ("duoserve", "oracle", "ondemand", "prefetchall"):
-            m, tl, _ = S.simulate_request(pol, trs, cfg, cost, net=pp)
+            m, tl = S.simulate_request(pol, trs, cfg, cost, net=pp)
             tl.check()                                   # seriality, weight-correctness, fetch-once
             assert m.ttft_s <= m.e2e_s and m.throughput_tokens_per_s > 0
             n_dec = sum(t.phase == "decode" for t in trs)
@@ -222,14 +222,14 @@ def test_cancellable_prefetch_extension():
     pp = PopularityPredictor(ST.build_popularity(ds), cfg.top_k)
     chunk = cfg.expert_bytes // 8
     for rid, trs in ds.by_request().items():
-        ms, tls, ls = S.simulate_request("duoserve", trs, cfg, cost, net=pp)
-        mc, tlc, lc = S.simulate_request("duoserve", trs, cfg, cost, net=pp, cancel_chunk_bytes=chunk)
+        ms, tls, ls = S.simulate_request("duoserve", trs, cfg, cost, net=pp, return_log=True)
+        mc, tlc, lc = S.simulate_request("duoserve", trs, cfg, cost, net=pp, cancel_chunk_bytes=chunk, return_log=True)
         assert lc == ls
         assert mc.e2e_s <= ms.e2e_s and mc.ttft_s <= ms.ttft_s
         assert mc.link_bytes <= ms.link_bytes
         tlc.check()
-        mo, _, _ = S.simulate_request("oracle", trs, cfg, cost)
-        mo2, _, _ = S.simulate_request("oracle", trs, cfg, cost, cancel_chunk_bytes=chunk)
+        mo, _ = S.simulate_request("oracle", trs, cfg, cost)
+        mo2, _ = S.simulate_request("oracle", trs, cfg, cost, cancel_chunk_bytes=chunk)
         assert mo2.e2e_s <= mo.e2e_s
         # with perfect predictions only the speculative prefill transfer differs
         assert abs((mo2.e2e_s - mo2.ttft_s) - (mo.e2e_s - mo.ttft_s)) < 1e-6
@@ -246,7 +246,7 @@ def test_b200_calibrated_preset():
     L = cfg.num_layers
     ds = T.generate_traces(T.default_generator_params(L, 8, 0.8, 3), cfg, 1, 4, 16)
     trs = ds.traces
-    m, tl, _ = S.simulate_request("oracle", trs, cfg, cost)
+    m, tl = S.simulate_request("oracle", trs, cfg, cost)
     per_tok = (m.e2e_s - m.ttft_s) / m.decode_tokens
     floor = L * cfg.top_k * cost.transfer_time_s(cfg.expert_bytes)
     assert floor <= per_tok < 1.2 * floor
@@ -281,3 +281,15 @@ def test_oracle_pinned_extension_properties():
         assert not pl & set(r.get("refetch", r.get("fetch", [])))
         n_pin += len(r["pinned"]) if r["layer"] > 0 else 0
     assert cnt["prefetch_hits"] + cnt["prefetch_misses"] + n_pin == cnt0["prefetch_hits"] + cnt0["prefetch_misses"]
+
+
+def test_simulate_request_returns_spec_pair():
+    """SPEC.md:365: simulate_request -> (RequestMetrics, EventTimeline); the
+    cache log is opt-in (return_log=True) and rides on the timeline."""
+    cfg = _cfg(2)
+    reqs = _req([((0, 1), (2, 3))], [((0, 1), (2, 3))])
+    out = S.simulate_request("ondemand", reqs, cfg, _cost(10, 2, 1))
+    assert len(out) == 2
+    m, tl = out
+    _, _, log = S.simulate_request("ondemand", reqs, cfg, _cost(10, 2, 1), return_log=True)
+    assert tl.cache_log == log and log
