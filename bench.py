@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--warmup-decode", type=int, default=None,
                     help="decode tokens per warm-up step (default: same as --decode)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true",
+                    help="skip the oracle check of the served request (routing, predicted sets, cache log)")
     ap.add_argument("--no-cancel", action="store_true",
                     help="paper-faithful decode: whole-expert prefetch, no cancellation of wrong prefetches")
     ap.add_argument("--chunk-mb", type=float, default=256.0,
@@ -222,6 +224,39 @@ def cpu_reference_sample(shape, prefill: int, budget_s: float = 20.0) -> dict:
                        f"{reps} decode tokens (gate + 2 experts + reference predictor step), scaled x{L} layers")}
 
 
+def parity_leg(eng, args, shape, net, pop, aff, timed: dict, one_step) -> dict:
+    """Checker leg (after the timed region; the oracle is test infrastructure):
+    the timed request's predicted sets and cache log vs oracle/predictor_ref +
+    oracle/sim_ref, then one more (untimed) serve of the same request with the
+    gate inputs captured: routing teacher-forced vs oracle/routing_ref, and
+    its cache log equal to the timed one (determinism)."""
+    from oracle import check_request, predictor_ref
+    L, k = shape.num_layers, shape.top_k
+    t0 = time.time()
+    ref_net = None
+    if args.policy == "duoserve":
+        # the served net through the reference's container format (predictor.py:577-646)
+        from paper_2509_07379_b200 import predictor as P
+        with tempfile.TemporaryDirectory() as td:
+            P.save_model(net, Path(td) / "net.bin")
+            ref_net = predictor_ref.load_container(Path(td) / "net.bin")
+    pol = "duoserve" if args.policy == "duoserve" else args.policy
+    out = {}
+    if args.policy in ("duoserve", "ondemand", "prefetchall") and not eng.ep:
+        out.update(check_request.check_request(timed["log"], timed["paths_prefill"], timed["paths_decode"], L, k,
+                                               ref_net, pop.values if pop is not None else None,
+                                               aff.values if aff is not None else None, policy=pol,
+                                               pinned=sorted(eng.pinned) or None))
+    eng.capture = []
+    rerun = one_step(len(timed["paths_decode"]))
+    cap, eng.capture = eng.capture, None
+    out["routing"] = check_request.check_routing(cap, [eng.W.layers[l]["wg"] for l in range(L)], k)
+    out["rerun_log_equal"] = rerun["log"] == timed["log"]
+    out["rerun_tokens_equal"] = rerun["tokens"] == timed["tokens"]
+    out["check_s"] = round(time.time() - t0, 1)
+    return out
+
+
 def predictor_ref_dim(shape):
     return shape.num_layers * shape.top_k + 2 * shape.num_experts + 1
 
@@ -330,7 +365,8 @@ def run_ours(args):
         return {"ttft_ms": e0.elapsed_time(e1), "decode_ms": e1.elapsed_time(e2),
                 "e2e_wall_ms": 1e3 * (w2 - w0), "ttft_wall_ms": 1e3 * (w1 - w0),
                 "h2d_experts": eng.h2d_bytes() - c0, "tokens": toks,
-                "d2h": eng.d2h_bytes}
+                "d2h": eng.d2h_bytes, "log": eng.log, "paths_prefill": eng.paths_prefill,
+                "paths_decode": eng.paths_decode}
 
     for _ in range(args.warmup):
         one_step(wd)
@@ -416,6 +452,8 @@ def run_ours(args):
         "setup_s": round(setup_s, 1),
         "predictor": eng.hit_summary(),
     }
+    if not args.no_parity and rank == 0:
+        line["parity"] = parity_leg(eng, args, shape, net, pop, aff, r0, one_step)
     if not args.no_cpu_baseline and ws == 1:
         cb = cpu_reference_sample(shape, args.prefill)
         v = cb["ttft_ms"] + args.decode * cb["decode_ms_per_token"]

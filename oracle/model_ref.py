@@ -105,19 +105,8 @@ class TinyMixtralRef:
         idx, w = self.gate(l, a)
         if idx_override is not None:
             idx = idx_override
-        T = h.shape[0]
-        acc = torch.zeros((T, s.hidden), dtype=torch.float32)
-        ws = torch.from_numpy(w)
-        for j in range(s.top_k):
-            for e in range(s.num_experts):
-                rows = np.nonzero(idx[:, j] == e)[0]
-                if rows.size == 0:
-                    continue
-                W1, W3, W2 = (self.exact if decode else self.rounded)[(l, e)]
-                x = a[rows]
-                hh = _bf(torch.nn.functional.silu(x @ W1.T) * (x @ W3.T))
-                y = hh @ W2.T
-                acc[rows] = acc[rows] + ws[rows, j:j + 1] * y
+        experts = [(self.exact if decode else self.rounded)[(l, e)] for e in range(s.num_experts)]
+        acc = moe_block(a, idx, w, experts)
         return _bf(h + acc), idx, a
 
     def forward(self, ids, decode: bool, idx_override=None):
@@ -131,3 +120,29 @@ class TinyMixtralRef:
         self.pos += len(ids)
         logits = _bf(self.norm(h[-1:], self.W.norm) @ self.W.lm_head.float())[0]
         return logits, idxs
+
+
+def moe_block(a: torch.Tensor, idx: np.ndarray, w: np.ndarray, experts, round_h: bool = True,
+              dtype=torch.float32) -> torch.Tensor:
+    """Routing-weighted SwiGLU expert sum of HF MixtralSparseMoeBlock
+    (modeling_mixtral.py:62-100: per selected expert SiLU(x W1^T) * (x W3^T),
+    then W2, times the routing weight, summed over the k slots in j order).
+    experts[e] = (W1 [ff, d], W3 [ff, d], W2 [d, ff]); round_h rounds the
+    SwiGLU intermediate to bf16 as the kernels do (K3/K4 write bf16 h)."""
+    T = a.shape[0]
+    d = experts[0][2].shape[0]
+    acc = torch.zeros((T, d), dtype=dtype)
+    ws = torch.from_numpy(np.asarray(w)).to(dtype)
+    x_all = a.to(dtype)
+    for j in range(idx.shape[1]):
+        for e in range(len(experts)):
+            rows = np.nonzero(idx[:, j] == e)[0]
+            if rows.size == 0:
+                continue
+            W1, W3, W2 = (m.to(dtype) for m in experts[e])
+            x = x_all[rows]
+            hh = torch.nn.functional.silu(x @ W1.T) * (x @ W3.T)
+            if round_h:
+                hh = _bf(hh).to(dtype)
+            acc[rows] = acc[rows] + ws[rows, j:j + 1] * (hh @ W2.T)
+    return acc

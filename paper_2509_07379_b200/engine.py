@@ -471,6 +471,8 @@ class Engine:
         self.route_stats = OnlineRoutingStats(self.L, self.M, self.k, dev) if collect_stats else None
         self.p_paths = torch.empty((P, self.L, self.k), dtype=torch.int32, device=dev) if collect_stats else None
         self.capture = None          # debug/parity: list of (phase, layer, gate input, idx)
+        self.capture_moe = None      # parity: set of layers whose MoE block in/out is recorded
+        self.moe_records = []        # dicts: phase, layer, token, h_in, a, out, idx, w (host copies)
         self.use_graphs = use_graphs
         self.g_graphs = None
         self.prof = None             # KernelProfiler when enabled (bench)
@@ -757,7 +759,9 @@ class Engine:
                     self.cache.load(slot2, l, e2)
         # next layer's first expert streams while this layer combines + next attention runs
         self._spec_fetch(l + 1)
-        return self._prefill_combine(h, T, w, idx), idx_host.numpy()
+        out = self._prefill_combine(h, T, w, idx)
+        self._record_moe("prefill", l, h, a, out, idx_host, w)
+        return out, idx_host.numpy()
 
     def _prefill_ffn(self, e: int, slot, off, st=None) -> None:
         lo, hi = off[e], off[e + 1]
@@ -787,7 +791,18 @@ class Engine:
         for e in A:
             self._prefill_ffn(e, self._pa_slot(self._pa_v, e), off)
         self._pa_done()
-        return self._prefill_combine(h, T, w, idx), idx_host.numpy()
+        out = self._prefill_combine(h, T, w, idx)
+        self._record_moe("prefill", l, h, rms_norm(h, self.W.layers[l]["ln2"], self.shape.rms_eps), out, idx_host, w)
+        return out, idx_host.numpy()
+
+    def _record_moe(self, phase: str, l: int, h, a, out, idx_host, w) -> None:
+        """Parity hook (tests / bench checker only): host copies of one MoE
+        block's input h, its normed gate input a, its output and the routing."""
+        if not self.capture_moe or l not in self.capture_moe:
+            return
+        self.moe_records.append({"phase": phase, "layer": l, "token": self.t_decode if phase == "decode" else None,
+                                 "h_in": h.cpu(), "a": a.cpu(), "out": out.cpu(),
+                                 "idx": torch.as_tensor(np.asarray(idx_host)).clone(), "w": w.cpu()})
 
     # --------------------------------------------------------------- decode
     def _moe_decode(self, l: int, h: torch.Tensor, pre: torch.Tensor | None = None, out: torch.Tensor | None = None):
@@ -820,7 +835,9 @@ class Engine:
             for e in mine:
                 self._decode_ffn(a, self.cache.acquire(self._pa_slot(self._pa_v, e)), E.index(e))
             self._pa_done()
-            return self._decode_combine(h, out), E
+            out = self._decode_combine(h, out)
+            self._record_moe("decode", l, h, a, out, self.idx_host, self.w1)
+            return out, E
         if l == 0 or not use_pred:
             base = 0 if (l % 2 == 0 or self.n_slots < 2 * self.k) else self.k
             for j, e in enumerate(mine):
@@ -858,6 +875,7 @@ class Engine:
             self._decode_ffn(a, self.cache.acquire(slot_of[e]), j)
             self.cache.release(slot_of[e])
         out = self._decode_combine(h, out)
+        self._record_moe("decode", l, h, a, out, self.idx_host, self.w1)
         # sync point 2: prediction for l+1 ready -> prefetch into the slots layer l-1 used
         if use_pred and l + 1 < self.L:
             Pn, order = self.driver.result(link)
