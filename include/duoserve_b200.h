@@ -12,8 +12,8 @@
  * Conventions (every function):
  *   - plain pointers and sizes only; device pointers are caller-owned
  *     (allocated by the caller, e.g. as torch tensors), "stream" is a
- *     cudaStream_t passed as void*; nothing allocates device memory except
- *     ds_cache_* (which owns its pinned/device buffers by design);
+ *     cudaStream_t passed as void*; no entry point allocates device memory
+ *     (the diagnostic DS_K4_TIMELINE / DS_K4_FUSED switches excepted);
  *   - return 0 on success, a positive cudaError_t on a CUDA failure, or a
  *     negative DS_ERR_* on invalid arguments; ds_last_error() returns the
  *     calling thread's last message;
@@ -179,6 +179,26 @@ int ds_w4_down_gemv(const void *h, int R, const ds_w4_expert *e, int d, int ff, 
 int ds_w4_expert_gemv(const void *x, int R, const ds_w4_expert *e, int d, int ff, int G, void *h,
                       const float *route_w, int route_stride, float *acc, void *ev_start, void *ev_end,
                       void *stream);
+/* ------------------------------------------------------------------------
+ * Plain W4 linears: the non-MoE projections (attention q|k|v and o) kept
+ * resident in HBM in the same W4 format, so the non-MoE weights fit the
+ * paper's W4 model budget ("2.15 GB"; SPEC.md:392-398 peak
+ * memory).  One blob per linear: codes | scales | zeros, each 256-B aligned.
+ * -------------------------------------------------------------------- */
+size_t ds_w4_linear_layout(int K, int N, int G, size_t offsets[3]);
+/* Counter-based init of one linear (tag < 64 names the matrix family; the
+ * experts use tags 0..M-1 via ds_w4_generate).                            */
+int ds_w4_generate_linear(uint64_t seed, int layer, int tag, int matrix, int K, int N, int G, void *blob,
+                          void *stream);
+/* y[R, N] (f32, overwritten) = x[R, K] (bf16) W^T for R <= 64 rows: the K4
+ * decode GEMV with routing weight 1 (exact (q - z) s products).           */
+int ds_w4_linear_gemv(const void *x, int R, const ds_w4_linear *w, int K, int N, int G, float *y,
+                      void *stream);
+/* Same for many rows on the tcgen05 GEMM (K3's down-projection kernel,
+ * bf16_rn((q - z) s) weights); workspace for the split-K partials.        */
+size_t ds_w4_linear_workspace(int rows, int K, int N);
+int ds_w4_linear_gemm(const void *x, int rows, const ds_w4_linear *w, int K, int N, int G, float *y,
+                      void *workspace, size_t workspace_bytes, void *stream);
 /* out[r] = bf16(resid[r] + acc[r]) and acc zeroed for the next layer.      */
 int ds_combine_finalize(float *acc, const void *resid, int R, int d, void *out, void *stream);
 /* Prefill grouped FFN (K3): for experts e in [0,E) (E <= 16): rows

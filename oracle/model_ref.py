@@ -12,7 +12,11 @@ their third-party sources so the B200 engine can be checked:
   * W4 dequant: w4_ref (vLLM awq_triton.py:54-101 rule).
 Prefill experts use bf16-rounded dequantised weights (what the tcgen05 GEMM
 consumes); decode experts use the exact (q - z) * s products (what the
-factorised GEMV computes) — see oracle/w4_ref.py.
+factorised GEMV computes) — see oracle/w4_ref.py.  The W4 attention
+projections (q|k|v fused, o; generator key (attn_seed, layer, ATTN_TAG,
+matrix)) follow the same rule by row count: <= GEMV_MAX_ROWS rows take the
+GEMV (exact products), more rows the GEMM (bf16-rounded weights); the o
+projection adds to the residual in f32 with one bf16 rounding.
 """
 
 from __future__ import annotations
@@ -25,6 +29,8 @@ import torch
 from . import routing_ref, w4_ref
 
 BF = torch.bfloat16
+ATTN_TAG, QKV_MATRIX, O_MATRIX = 63, 0, 1     # restated from paper_2509_07379_b200/model.py
+GEMV_MAX_ROWS = 16                            # rows at or below which the product uses the GEMV
 
 
 def _bf(x: torch.Tensor) -> torch.Tensor:
@@ -53,6 +59,15 @@ class TinyMixtralRef:
                 self.rounded[(l, e)] = r          # [N, K] each
                 self.exact[(l, e)] = x
         hd = shape.head_dim
+        self.attn = {}                            # (layer, name) -> (rounded [N, K], exact [N, K])
+        aseed = getattr(dense, "attn_seed", 0)
+        for l in range(shape.num_layers):
+            for name, m, K, N in (("wqkv", QKV_MATRIX, d, (shape.n_heads + 2 * shape.n_kv_heads) * hd),
+                                  ("wo", O_MATRIX, shape.n_heads * hd, d)):
+                c, sc, z = w4_ref.gen_linear(aseed, l, ATTN_TAG, m, K, N, G)
+                self.attn[(l, name)] = (torch.from_numpy(w4_ref.bf16_bits_to_f32(w4_ref.dequant(c, sc, z, K, N, G))),
+                                        torch.from_numpy(w4_ref.dequant_exact(c, sc, z, K, N, G)).float())
+        hd = shape.head_dim
         inv = 1.0 / (shape.rope_theta ** (torch.arange(0, hd, 2, dtype=torch.float32) / hd))
         f = torch.outer(torch.arange(4096, dtype=torch.float32), inv)
         emb = torch.cat([f, f], -1)
@@ -75,14 +90,20 @@ class TinyMixtralRef:
         rot = torch.cat([-x[..., h:], x[..., :h]], -1)
         return _bf(x * c + rot * s)
 
+    def _w(self, l, name, rows):
+        r, x = self.attn[(l, name)]
+        return x if rows <= GEMV_MAX_ROWS else r
+
     def attn(self, l, h):
         s = self.s
         Lw = self.W.layers[l]
         T = h.shape[0]
         a = self.norm(h, Lw["ln1"])
-        q = _bf(a @ Lw["wq"].float()).view(T, s.n_heads, s.head_dim)
-        k = _bf(a @ Lw["wk"].float()).view(T, s.n_kv_heads, s.head_dim)
-        v = _bf(a @ Lw["wv"].float()).view(T, s.n_kv_heads, s.head_dim)
+        nh, nkv, hd = s.n_heads, s.n_kv_heads, s.head_dim
+        y = _bf(a @ self._w(l, "wqkv", T).T)
+        q = y[:, : nh * hd].reshape(T, nh, hd)
+        k = y[:, nh * hd:(nh + nkv) * hd].reshape(T, nkv, hd)
+        v = y[:, (nh + nkv) * hd:].reshape(T, nkv, hd)
         q, k = self.rope(q, self.pos), self.rope(k, self.pos)
         self.K[l] = k if self.K[l] is None else torch.cat([self.K[l], k])
         self.V[l] = v if self.V[l] is None else torch.cat([self.V[l], v])
@@ -93,7 +114,7 @@ class TinyMixtralRef:
         causal = torch.arange(n)[None, :] <= (torch.arange(T)[:, None] + self.pos)
         S = S.masked_fill(~causal[None], float("-inf"))
         o = _bf(torch.einsum("hts,shd->thd", torch.softmax(S, -1), Vx)).reshape(T, -1)
-        return _bf(h + _bf(o @ Lw["wo"].float()))
+        return _bf(h + o @ self._w(l, "wo", T).T)
 
     def gate(self, l, a):
         lg = routing_ref.gate_logits(_bits(a), _bits(self.W.layers[l]["wg"]))

@@ -82,6 +82,11 @@ _SIGS = {
     "ds_w4_expert_gemv": (_I, [_P, _I, C.POINTER(W4Expert), _I, _I, _I, _P, _P, _I, _P, _P, _P, _P]),
     "ds_combine_finalize": (_I, [_P, _P, _I, _I, _P, _P]),
     "ds_w4_grouped_ffn_workspace": (_SZ, [_I, _I, _I]),
+    "ds_w4_linear_layout": (_SZ, [_I, _I, _I, C.POINTER(_SZ * 3)]),
+    "ds_w4_generate_linear": (_I, [C.c_uint64, _I, _I, _I, _I, _I, _I, _P, _P]),
+    "ds_w4_linear_gemv": (_I, [_P, _I, C.POINTER(W4Linear), _I, _I, _I, _P, _P]),
+    "ds_w4_linear_workspace": (_SZ, [_I, _I, _I]),
+    "ds_w4_linear_gemm": (_I, [_P, _I, C.POINTER(W4Linear), _I, _I, _I, _P, _P, _SZ, _P]),
     "ds_link_create": (_I, [_P, _SZ, _I, C.POINTER(_P)]),
     "ds_link_destroy": (_I, [_P]),
     "ds_link_submit": (_I, [_P, _P, _P, _SZ, _P, _P, C.POINTER(C.c_uint64)]),

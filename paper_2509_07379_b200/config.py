@@ -243,8 +243,10 @@ class ModelShape:
 
     @property
     def attn_bytes_per_layer(self) -> int:
+        """W4 q|k|v and o projections (the paper's W4 model)."""
         d, hd = self.hidden, self.head_dim
-        return 2 * (d * self.n_heads * hd * 2 + d * self.n_kv_heads * hd * 2)
+        return (self.w4_matrix_bytes(d, (self.n_heads + 2 * self.n_kv_heads) * hd)
+                + self.w4_matrix_bytes(self.n_heads * hd, d))
 
     @property
     def non_moe_bytes(self) -> int:

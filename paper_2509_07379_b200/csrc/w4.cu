@@ -888,6 +888,60 @@ extern "C" int ds_w4_generate(uint64_t seed, int layer, int expert, int d, int f
     return DS_OK;
 }
 
+extern "C" size_t ds_w4_linear_layout(int K, int N, int G, size_t offsets[3]) {
+    if (K <= 0 || N <= 0 || G <= 0 || K % G || G % 32 || K % 8) return 0;
+    const size_t sizes[3] = {(size_t)N * K / 2, (size_t)N * (K / G) * 2, ((size_t)N * (K / G) + 1) / 2};
+    size_t off = 0;
+    for (int i = 0; i < 3; ++i) {
+        if (offsets) offsets[i] = off;
+        off = align_up(off + sizes[i]);
+    }
+    return off;
+}
+
+extern "C" int ds_w4_generate_linear(uint64_t seed, int layer, int tag, int matrix, int K, int N, int G, void* blob,
+                                     void* stream) {
+    size_t off[3];
+    DS_CHECK_ARG(ds_w4_linear_layout(K, N, G, off) > 0, "ds_w4_generate_linear: bad shape K=%d N=%d G=%d", K, N, G);
+    DS_CHECK_ARG(blob && ((uintptr_t)blob & 255) == 0, "ds_w4_generate_linear: blob must be 256B aligned");
+    DS_CHECK_ARG(layer >= 0 && tag >= 0 && tag < 64 && matrix >= 0 && matrix < 4,
+                 "ds_w4_generate_linear: bad layer/tag/matrix");
+    cudaStream_t st = as_stream(stream);
+    char* base = static_cast<char*>(blob);
+    const int grid = 4 * num_sms();
+    const size_t words = (size_t)N * K / 8, groups = (size_t)N * (K / G);
+    gen_codes_kernel<<<grid, 256, 0, st>>>(stream_key(seed, layer, tag, matrix, 0), words, (uint32_t*)(base + off[0]));
+    gen_scales_kernel<<<grid, 256, 0, st>>>(stream_key(seed, layer, tag, matrix, 2), groups, K,
+                                            (uint16_t*)(base + off[1]));
+    gen_zeros_kernel<<<grid, 256, 0, st>>>(stream_key(seed, layer, tag, matrix, 1), (groups + 1) / 2,
+                                           (uint8_t*)(base + off[2]));
+    DS_LAUNCH_CHECK("ds_w4_generate_linear");
+    return DS_OK;
+}
+
+__device__ const float g_one_f32 = 1.0f;
+
+// Plain W4 linear for a few rows (decode attention projections): y = x W^T
+// through the decode down-GEMV (K4) with routing weight 1 into a zeroed y.
+extern "C" int ds_w4_linear_gemv(const void* x, int R, const ds_w4_linear* w, int K, int N, int G, float* y,
+                                 void* stream) {
+    DS_CHECK_ARG(w && check_linear(*w) && x && y, "ds_w4_linear_gemv: NULL pointer");
+    DS_CHECK_ARG(R >= 1 && R <= 64, "ds_w4_linear_gemv: 1 <= R <= 64");
+    cudaStream_t st = as_stream(stream);
+    static const float* one = nullptr;
+    if (!one) {
+        void* p = nullptr;
+        cudaError_t e = cudaGetSymbolAddress(&p, g_one_f32);
+        if (e != cudaSuccess) return cuda_status(e, "ds_w4_linear_gemv: constant");
+        one = static_cast<const float*>(p);
+    }
+    cudaError_t e = cudaMemsetAsync(y, 0, (size_t)R * N * sizeof(float), st);
+    if (e != cudaSuccess) return cuda_status(e, "ds_w4_linear_gemv: zero y");
+    ds_w4_expert ex{};
+    ex.w2 = *w;
+    return ds_w4_down_gemv(x, R, &ex, N, K, G, one, 0, y, stream);
+}
+
 extern "C" int ds_w4_dequant(const ds_w4_linear* w, int K, int N, int G, void* out, void* stream) {
     DS_CHECK_ARG(w && check_linear(*w) && out, "ds_w4_dequant: NULL pointer");
     DS_CHECK_ARG(K > 0 && N > 0 && G > 0 && K % G == 0 && G % 8 == 0, "ds_w4_dequant: bad shape");
@@ -1258,6 +1312,8 @@ static int down_staged(const __nv_bfloat16* h, const ds_w4_expert* e, int d, int
     if (rb == 0) return 1;                                                                   // v2 down
 #define DS_DN(CPL, RB) staged_launch<1, CPL, G, RB, false>(h, to_ptr(e->w2), to_ptr(e->w2), d, nullptr, rw, acc, st)
     switch (ff / 1024) {
+        case 4: return DS_DN(4, 4);          // W4 attention projections (8x7B: K = 4096)
+        case 6: return DS_DN(6, 4);          // (8x22B: K = 6144)
         case 14: return rb == 2 ? DS_DN(14, 2) : rb == 8 ? DS_DN(14, 8) : DS_DN(14, 4);
         case 16: return rb == 2 ? DS_DN(16, 2) : rb == 8 ? DS_DN(16, 8) : DS_DN(16, 4);
         default: return 1;

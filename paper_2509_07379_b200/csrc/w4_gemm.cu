@@ -590,3 +590,58 @@ static int grouped_ffn_impl(const void* xperm, const int32_t* offsets, int E, co
     }
     return DS_OK;
 }
+
+// Plain W4 linear for many rows (prefill attention projections): y[rows, N]
+// (f32) = x[rows, K] W^T on the same tcgen05 kernel as the expert down
+// projection (NMAT = 1: one weight matrix, f32 output, split-K with the fixed-
+// order reduction when the tile count alone cannot fill the SMs).
+extern "C" size_t ds_w4_linear_workspace(int rows, int K, int N) {
+    int s = 1;
+    for (int tn : {128, 256})
+        for (int g : {64, 128}) {
+            const int v = ds::splits_for(N, K, g, (rows + tn - 1) / tn);
+            s = v > s ? v : s;
+        }
+    return s > 1 ? (size_t)s * rows * N * sizeof(float) : 0;
+}
+
+extern "C" int ds_w4_linear_gemm(const void* x, int rows, const ds_w4_linear* w, int K, int N, int G, float* y,
+                                 void* workspace, size_t workspace_bytes, void* stream) {
+    DS_CHECK_ARG(x && w && w->codes && w->scales && w->zeros && y, "ds_w4_linear_gemm: NULL pointer");
+    DS_CHECK_ARG(rows >= 0 && N % BM == 0 && K % BK == 0 && (G == 64 || G == 128) && K % G == 0,
+                 "ds_w4_linear_gemm: need N %% 128 == 0, K %% 64 == 0, G in {64, 128}");
+    if (rows == 0) return DS_OK;
+    const int TN = rows > 128 ? 256 : 128;
+    const int mb = (rows + TN - 1) / TN;
+    GemmArgs a{};
+    a.row_start[0] = 0;
+    a.rows[0] = rows;
+    a.w[0][0] = W4Mat{w->codes, (const uint16_t*)w->scales, w->zeros};
+    int rc = make_codes_map(&a.codes_map[0][0], w->codes, N, K);
+    if (rc) return rc;
+    CUtensorMap map;
+    rc = make_act_map(&map, x, rows, K, TN);
+    if (rc) return rc;
+    const int splits = splits_for(N, K, G, mb);
+    DS_CHECK_ARG((K / splits) / G + 2 <= kMaxGroupsPerCta, "ds_w4_linear_gemm: K / G too large");
+    a.K = K; a.N = N; a.G = G; a.kt_per_split = (K / BK) / splits; a.splits = splits; a.total_rows = rows;
+    const size_t need = (size_t)splits * rows * N * sizeof(float);
+    if (splits == 1) {
+        a.out = y;
+    } else {
+        if (!workspace || workspace_bytes < need)
+            return fail(DS_ERR_WORKSPACE, "ds_w4_linear_gemm: workspace %zu < %zu", workspace_bytes, need);
+        a.out = workspace;
+    }
+    cudaStream_t st = as_stream(stream);
+    rc = TN == 256 ? launch_gemm<1, 256>(map, a, 1, mb, st) : launch_gemm<1, 128>(map, a, 1, mb, st);
+    if (rc) return rc;
+    if (splits > 1) {
+        const size_t n = (size_t)rows * N;
+        int grid = (int)((n + 255) / 256);
+        if (grid > 4 * num_sms()) grid = 4 * num_sms();
+        split_reduce_kernel<<<grid, 256, 0, st>>>(static_cast<const float*>(workspace), splits, n, y);
+        DS_LAUNCH_CHECK("ds_w4_linear_gemm: split reduce");
+    }
+    return DS_OK;
+}

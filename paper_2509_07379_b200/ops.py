@@ -162,3 +162,65 @@ def route_histogram(paths: torch.Tensor, M: int, pop_counts: torch.Tensor, aff_c
     N, L, k = paths.shape
     _lib.call("ds_route_histogram", ptr(paths), N, L, M, k, ptr(pop_counts), ptr(aff_counts), stream_ptr())
     _count("ds_route_histogram")
+
+
+# ------------------------------------------------------------- W4 linears
+# the non-MoE projections (attention q|k|v, o) in the experts' W4 format
+
+@lru_cache(maxsize=None)
+def linear_layout(K: int, N: int, G: int):
+    """(section offsets [codes, scales, zeros], total bytes) of one W4 linear blob."""
+    offs = (C.c_size_t * 3)()
+    total = _lib.query("ds_w4_linear_layout", K, N, G, C.byref(offs))
+    if total == 0:
+        raise ValueError(f"unsupported W4 linear shape K={K} N={N} G={G}")
+    return tuple(offs), int(total)
+
+
+class W4Lin:
+    """One resident W4 linear y = x W^T (W [N, K]): its device blob + the C struct."""
+
+    def __init__(self, blob: torch.Tensor, K: int, N: int, G: int):
+        offs, total = linear_layout(K, N, G)
+        if blob.numel() < total or blob.dtype != torch.uint8:
+            raise ValueError("W4Lin: blob too small")
+        self.blob, self.K, self.N, self.G = blob, K, N, G
+        self.st = _lib.W4Linear()
+        base = blob.data_ptr()
+        self.st.codes, self.st.scales, self.st.zeros = base + offs[0], base + offs[1], base + offs[2]
+
+    @classmethod
+    def generate(cls, seed: int, layer: int, tag: int, matrix: int, K: int, N: int, G: int, device) -> "W4Lin":
+        _, total = linear_layout(K, N, G)
+        blob = torch.empty(total, dtype=torch.uint8, device=device)
+        _lib.call("ds_w4_generate_linear", seed, layer, tag, matrix, K, N, G, ptr(blob), stream_ptr())
+        _count("ds_w4_generate_linear", 3)
+        return cls(blob, K, N, G)
+
+    @property
+    def nbytes(self) -> int:
+        return self.blob.numel()
+
+
+def linear_workspace(rows: int, K: int, N: int) -> int:
+    return int(_lib.query("ds_w4_linear_workspace", rows, K, N))
+
+
+GEMV_MAX_ROWS = 16      # rows at or below which the GEMV (K4) path is used
+
+
+def w4_linear(x: torch.Tensor, lin: W4Lin, y: torch.Tensor, ws: torch.Tensor | None = None) -> torch.Tensor:
+    """y[R, N] (f32) = x[R, K] (bf16) W^T: the K4 GEMV for R <= GEMV_MAX_ROWS
+    (exact (q - z) s products), the tcgen05 GEMM above (bf16-rounded weights)."""
+    R = x.shape[0]
+    if x.shape[1] != lin.K or y.shape[0] < R or y.shape[1] != lin.N:
+        raise ValueError(f"w4_linear: x {tuple(x.shape)} / y {tuple(y.shape)} vs W [{lin.N}, {lin.K}]")
+    if R <= GEMV_MAX_ROWS:
+        _lib.call("ds_w4_linear_gemv", ptr(x), R, C.byref(lin.st), lin.K, lin.N, lin.G, ptr(y), stream_ptr())
+        _count("ds_w4_linear_gemv", _gemv_passes(R, lin.G))
+    else:
+        nb = ws.numel() if ws is not None else 0
+        _lib.call("ds_w4_linear_gemm", ptr(x), R, C.byref(lin.st), lin.K, lin.N, lin.G, ptr(y), ptr(ws), nb,
+                  stream_ptr())
+        _count("ds_w4_linear_gemm", 2)
+    return y

