@@ -59,13 +59,13 @@ class TinyMixtralRef:
                 self.rounded[(l, e)] = r          # [N, K] each
                 self.exact[(l, e)] = x
         hd = shape.head_dim
-        self.attn = {}                            # (layer, name) -> (rounded [N, K], exact [N, K])
+        self.attn_w = {}                          # (layer, name) -> (rounded [N, K], exact [N, K])
         aseed = getattr(dense, "attn_seed", 0)
         for l in range(shape.num_layers):
             for name, m, K, N in (("wqkv", QKV_MATRIX, d, (shape.n_heads + 2 * shape.n_kv_heads) * hd),
                                   ("wo", O_MATRIX, shape.n_heads * hd, d)):
                 c, sc, z = w4_ref.gen_linear(aseed, l, ATTN_TAG, m, K, N, G)
-                self.attn[(l, name)] = (torch.from_numpy(w4_ref.bf16_bits_to_f32(w4_ref.dequant(c, sc, z, K, N, G))),
+                self.attn_w[(l, name)] = (torch.from_numpy(w4_ref.bf16_bits_to_f32(w4_ref.dequant(c, sc, z, K, N, G))),
                                         torch.from_numpy(w4_ref.dequant_exact(c, sc, z, K, N, G)).float())
         hd = shape.head_dim
         inv = 1.0 / (shape.rope_theta ** (torch.arange(0, hd, 2, dtype=torch.float32) / hd))
@@ -91,7 +91,7 @@ class TinyMixtralRef:
         return _bf(x * c + rot * s)
 
     def _w(self, l, name, rows):
-        r, x = self.attn[(l, name)]
+        r, x = self.attn_w[(l, name)]
         return x if rows <= GEMV_MAX_ROWS else r
 
     def attn(self, l, h):
