@@ -56,8 +56,18 @@ def parse():
     ap.add_argument("--chunk-mb", type=float, default=256.0,
                     help="chunk size of confirmed transfers (re-fetches, promoted prefetches); >= the expert = whole-expert copies")
     ap.add_argument("--link-depth", type=int, default=2)
-    ap.add_argument("--pin-mb", type=float, default=0.0,
-                    help="residency-budget policy: HBM (MiB) for the most popular experts, pinned for the request")
+    ap.add_argument("--pin-mb", type=float, default=-1.0,
+                    help="residency-budget policy: HBM (MiB) for the most popular experts, pinned for the request; "
+                         "-1 (default) = whatever keeps the measured peak under the residency cap, 0 = off")
+    ap.add_argument("--residency-cap", type=float, default=0.15,
+                    help="peak device bytes / W4 model bytes the auto pin budget stays under (PAPER: ~15 %%)")
+    ap.add_argument("--predictor", default="trained", choices=["trained", "random"],
+                    help="trained: the paper's preprocess on this model (serve calibration prompts on-demand, "
+                         "count pop/aff on the GPU, train the ExpertMLP on the GPU); random: ExpertMLP(seed=0) "
+                         "with pop/aff from synthetic traces (SURVEY.md §8d)")
+    ap.add_argument("--calib-requests", type=int, default=4)
+    ap.add_argument("--calib-decode", type=int, default=32)
+    ap.add_argument("--train-epochs", type=int, default=15)
     ap.add_argument("--spec-chunk-mb", type=float, default=0.5,
                     help="chunk size of speculative (predicted) prefetches until the gate confirms them")
     ap.add_argument("--seed", type=int, default=0)
@@ -257,6 +267,41 @@ def parity_leg(eng, args, shape, net, pop, aff, timed: dict, one_step) -> dict:
     return out
 
 
+def calibrate(shape, args, serve_kw, store, rank, ws, ep):
+    """The paper's preprocess on the served model:
+    serve --calib-requests prompts (seeds disjoint from the timed request's)
+    with on-demand scheduling while the gate's device counters record
+    popularity / affinity, train the ExpertMLP on the GPU, evaluate it on the
+    held-out requests.  Returns (PreprocessResult, dense weights, store) so
+    the serving engine reuses the weights and the pinned expert store."""
+    import torch
+    from paper_2509_07379_b200.engine import Engine
+    from paper_2509_07379_b200.preprocess import preprocess
+    col = Engine(shape, "ondemand", store=store, collect_stats=True, **serve_kw)
+    g = torch.Generator().manual_seed(10_000 + args.seed + (0 if ep else 1000 * rank))
+    prompts = [torch.randint(0, shape.vocab, (args.prefill,), generator=g) for _ in range(args.calib_requests)]
+    pre = preprocess(col, prompts, args.calib_decode, epochs=args.train_epochs, seed=args.seed)
+    if ep is not None and ws > 1:
+        # every rank saw the same routing; serve rank 0's net everywhere (bitwise identical predictions)
+        import torch.distributed as dist
+        obj = [pre if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        pre = obj[0]
+    dense, store = col.W, col.store
+    col.close()
+    del col
+    torch.cuda.empty_cache()
+    return pre, dense, store
+
+
+def preprocess_summary(pre, shape) -> dict:
+    r = pre.train_report
+    return {"table": pre.table(shape.name), "timings_s": pre.timings_s, "n_traces": pre.n_traces,
+            "train": {"epochs": r.epochs, "n_samples": r.n_samples, "batch_size": r.batch_size,
+                      "first_loss": round(r.epoch_losses[0], 5) if r.epoch_losses else None,
+                      "last_loss": round(r.epoch_losses[-1], 5) if r.epoch_losses else None}}
+
+
 def predictor_ref_dim(shape):
     return shape.num_layers * shape.top_k + 2 * shape.num_experts + 1
 
@@ -307,8 +352,6 @@ def run_ours(args):
     if args.pin_mb > 0 and args.policy == "prefetchall":
         raise SystemExit("--pin-mb does not apply to --policy prefetchall (every expert is streamed by design)")
     wd = args.warmup_decode if args.warmup_decode is not None else args.decode
-    net, pop, aff = predictor_inputs(shape) if args.policy in ("duoserve", "oracle") or args.pin_mb > 0 \
-        else (None, None, None)
     # replicas: an independent request per rank; EP: every rank serves the same request
     gen = torch.Generator().manual_seed(args.seed + (0 if args.ep else 1000 * rank))
     ids_host = torch.randint(0, shape.vocab, (args.prefill,), generator=gen).pin_memory()
@@ -325,21 +368,31 @@ def run_ours(args):
         if len(members) > 1:
             store = HostExpertStore(shape, args.seed, dev, shared_group=grp)
     n_record = max(args.decode, wd)
-    serve_kw = dict(seed=args.seed, device=dev, ep=ep, max_seq=args.prefill + n_record + 8,
+    serve_kw = dict(seed=args.seed, device=dev, ep=ep, max_seq=args.prefill + max(n_record, args.calib_decode) + 8,
                     max_prefill=args.prefill, cancel_mispredicted=not args.no_cancel, chunk_mb=args.chunk_mb,
-                    link_depth=args.link_depth, spec_chunk_mb=args.spec_chunk_mb,
-                    pin_budget_bytes=int(args.pin_mb * 2**20))
+                    link_depth=args.link_depth, spec_chunk_mb=args.spec_chunk_mb)
+    needs_stats = args.policy in ("duoserve", "oracle") or (args.pin_mb != 0 and args.policy != "prefetchall")
+    pre = None
+    dense = None
+    if needs_stats and args.predictor == "trained" and args.policy != "prefetchall":
+        # the paper's preprocess on this model, on this GPU
+        pre, dense, store = calibrate(shape, args, serve_kw, store, rank, ws, ep)
+        net, pop, aff = pre.net, pre.pop, pre.aff
+    elif needs_stats:
+        net, pop, aff = predictor_inputs(shape)
+    else:
+        net, pop, aff = None, None, None
     if args.policy == "oracle":
         # record the routing once with the predictor-driven engine, then replay
         # it as the perfect predictor (SPEC DuoServeOracle) on the same weights
-        rec = Engine(shape, "duoserve", store=store, predictor=net, pop=pop, aff=aff, **serve_kw)
+        rec = Engine(shape, "duoserve", dense=dense, store=store, predictor=net, pop=pop, aff=aff, **serve_kw)
         rec.reset()
         rec.generate(ids_host, n_record + 1)
         eng = Engine(shape, "oracle", dense=rec.W, store=rec.store, oracle_paths=rec.paths_decode, pop=pop,
                      **serve_kw)
         del rec
     else:
-        eng = Engine(shape, args.policy, store=store, predictor=net, pop=pop, aff=aff, **serve_kw)
+        eng = Engine(shape, args.policy, dense=dense, store=store, predictor=net, pop=pop, aff=aff, **serve_kw)
     setup_s = time.time() - t_setup
     prof = eng.enable_profile()
     eng.link_peak_gbs()
@@ -368,7 +421,20 @@ def run_ours(args):
                 "d2h": eng.d2h_bytes, "log": eng.log, "paths_prefill": eng.paths_prefill,
                 "paths_decode": eng.paths_decode}
 
-    for _ in range(args.warmup):
+    # first warm-up step without pinned experts: its peak sizes the residency budget
+    torch.cuda.synchronize()
+    torch.cuda.reset_peak_memory_stats(dev)
+    one_step(wd)
+    base_peak = torch.cuda.max_memory_allocated(dev)
+    pin_info = {"budget_bytes": 0, "experts": 0}
+    if args.pin_mb != 0 and args.policy != "prefetchall":
+        cap_bytes = int(args.residency_cap * shape.total_bytes)
+        budget = int(args.pin_mb * 2**20) if args.pin_mb > 0 else cap_bytes - base_peak - (64 << 20)
+        n_pin = eng.pin_experts(pop, budget) if budget > 0 else 0
+        pin_info = {"budget_bytes": max(budget, 0), "experts": n_pin, "peak_before_pinning": int(base_peak),
+                    "cap_bytes": cap_bytes, "chosen_by": "popularity measured on this model's calibration requests"
+                    if pre is not None else "popularity of the synthetic traces"}
+    for _ in range(max(args.warmup - 1, 0)):
         one_step(wd)
     prof.reset()
     torch.cuda.reset_peak_memory_stats(dev)     # residency = peak of the serving loop, not of setup
@@ -450,7 +516,9 @@ def run_ours(args):
                 "d2h_bytes_per_step": int(r0["d2h"])},
         "clocks": clk.summary(),
         "setup_s": round(setup_s, 1),
-        "predictor": eng.hit_summary(),
+        "predictor": {**eng.hit_summary(), "source": args.predictor,
+                      **({"preprocess": preprocess_summary(pre, shape)} if pre is not None else {})},
+        "pinning": pin_info,
     }
     if not args.no_parity and rank == 0:
         line["parity"] = parity_leg(eng, args, shape, net, pop, aff, r0, one_step)

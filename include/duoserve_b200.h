@@ -256,6 +256,13 @@ int ds_link_trace(ds_link *link, int enable);
 int ds_link_trace_read(ds_link *link, void *ref_event, float *start_ms, float *end_ms, size_t max_spans,
                        size_t *n_out);
 
+/* SM-driven host->HBM copy: `ctas` CTAs stream `bytes` from mapped pinned host
+ * memory (cudaHostAlloc / cudaHostRegister, UVA) over PCIe with 16-byte loads
+ * and streaming stores into `dst` on `stream`.  An alternative to the copy
+ * engine for the expert link (PAPER.md:177-188 prescribes only "a dedicated
+ * communication stream"); 16-byte aligned pointers and size. */
+int ds_h2d_sm_copy(void *dst, const void *src_host, size_t bytes, int ctas, void *stream);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -30,6 +30,18 @@ inline int cuda_status(cudaError_t e, const char* what) {
 
 int num_sms();
 
+// ---- launch gate (measurement hygiene for CUDA-event kernel spans) -------
+// A span [ev_start, ev_end] recorded on an idle stream around host-side
+// launches also contains the host's submission latency (the start event fires
+// as soon as it is recorded, the kernel only once the host has submitted it).
+// gate_hold() makes the stream wait (cuStreamWaitValue32 on a device word)
+// until gate_release() — issued after every launch of the span is queued —
+// so the span covers device execution only.  Returns 0 when the stream memory
+// operations are unavailable (then the span is recorded ungated).
+// DS_LAUNCH_GATE=0 disables it (A/B runs).
+unsigned gate_hold(cudaStream_t st);
+void gate_release(unsigned seq);
+
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 // ---- counter-based generator (splitmix64 finaliser) ---------------------

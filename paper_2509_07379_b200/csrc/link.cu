@@ -331,3 +331,50 @@ extern "C" int ds_link_trace_read(ds_link* L, void* ref_event, float* start_ms, 
     if (err) return fail(err, "ds_link_trace_read: cudaEventElapsedTime failed: %s", cudaGetErrorString((cudaError_t)err));
     return DS_OK;
 }
+
+// ---------------------------------------------------------------------------
+// SM-driven host->HBM copy (experiment: an alternative to the copy engine for
+// the expert link).  Pinned host memory is mapped into the device's address
+// space (UVA), so a kernel can stream it over PCIe with ordinary loads.  Each
+// thread keeps U 16-byte loads in flight; stores to HBM are streaming (.cs).
+namespace ds_zc {
+constexpr int kZcThreads = 256;
+constexpr int kZcU = 8;
+
+__global__ void __launch_bounds__(kZcThreads) zc_copy_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src,
+                                                             size_t n16) {
+    const size_t stride = (size_t)gridDim.x * kZcThreads * kZcU;
+    for (size_t base = (size_t)blockIdx.x * kZcThreads * kZcU + threadIdx.x; base < n16; base += stride) {
+        uint4 v[kZcU];
+#pragma unroll
+        for (int u = 0; u < kZcU; ++u) {
+            const size_t i = base + (size_t)u * kZcThreads;
+            if (i < n16) {
+                const uint4* p = src + i;
+                asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                             : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w) : "l"(p));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kZcU; ++u) {
+            const size_t i = base + (size_t)u * kZcThreads;
+            if (i < n16) __stcs(dst + i, v[u]);
+        }
+    }
+}
+}  // namespace ds_zc
+
+extern "C" int ds_h2d_sm_copy(void* dst, const void* src_host, size_t bytes, int ctas, void* stream) {
+    DS_CHECK_ARG(dst && src_host, "ds_h2d_sm_copy: NULL pointer");
+    DS_CHECK_ARG(bytes % 16 == 0 && ((uintptr_t)dst & 15) == 0 && ((uintptr_t)src_host & 15) == 0,
+                 "ds_h2d_sm_copy: pointers and size must be 16-byte aligned");
+    DS_CHECK_ARG(ctas > 0 && ctas <= 4096, "ds_h2d_sm_copy: ctas=%d", ctas);
+    void* dsrc = nullptr;
+    cudaError_t e = cudaHostGetDevicePointer(&dsrc, const_cast<void*>(src_host), 0);
+    if (e != cudaSuccess) return cuda_status(e, "ds_h2d_sm_copy: source is not mapped pinned host memory");
+    if (bytes == 0) return DS_OK;
+    ds_zc::zc_copy_kernel<<<ctas, ds_zc::kZcThreads, 0, ds::as_stream(stream)>>>(static_cast<uint4*>(dst),
+                                                                  static_cast<const uint4*>(dsrc), bytes / 16);
+    DS_LAUNCH_CHECK("ds_h2d_sm_copy");
+    return DS_OK;
+}

