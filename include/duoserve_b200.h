@@ -262,6 +262,9 @@ int ds_link_trace_read(ds_link *link, void *ref_event, float *start_ms, float *e
  * engine for the expert link (PAPER.md:177-188 prescribes only "a dedicated
  * communication stream"); 16-byte aligned pointers and size. */
 int ds_h2d_sm_copy(void *dst, const void *src_host, size_t bytes, int ctas, void *stream);
+/* Same contract, moved by TMA bulk copies (one thread per CTA, a shared-memory
+ * ring of 32 KB chunks): a few CTAs keep the PCIe reads in flight. */
+int ds_h2d_tma_copy(void *dst, const void *src_host, size_t bytes, int ctas, void *stream);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

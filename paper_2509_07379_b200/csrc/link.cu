@@ -15,6 +15,7 @@
 // compute), then the chunks are issued, then `done_event` is recorded (the
 // slot's ready event, waited on by the compute stream).
 #include "ds_common.cuh"
+#include "sm100.cuh"
 
 #include <atomic>
 #include <chrono>
@@ -376,5 +377,80 @@ extern "C" int ds_h2d_sm_copy(void* dst, const void* src_host, size_t bytes, int
     ds_zc::zc_copy_kernel<<<ctas, ds_zc::kZcThreads, 0, ds::as_stream(stream)>>>(static_cast<uint4*>(dst),
                                                                   static_cast<const uint4*>(dsrc), bytes / 16);
     DS_LAUNCH_CHECK("ds_h2d_sm_copy");
+    return DS_OK;
+}
+
+// TMA-driven host->HBM copy: one thread per CTA streams CH-byte chunks from
+// mapped pinned host memory into a shared-memory ring with cp.async.bulk
+// (mbarrier transaction counts) and writes each back to HBM with a bulk
+// shared->global store, so a handful of SMs (no per-byte instructions) keep
+// ~ring-size bytes of PCIe reads in flight.
+namespace ds_zc {
+constexpr int kTmaChunk = 32 * 1024;
+constexpr int kTmaSlots = 6;
+
+__global__ void __launch_bounds__(32) tma_copy_kernel(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src,
+                                                      size_t bytes) {
+    using namespace ds::sm100;
+    extern __shared__ __align__(128) uint8_t ring[];
+    __shared__ __align__(8) uint64_t full[kTmaSlots];
+    if (threadIdx.x != 0) return;
+    for (int i = 0; i < kTmaSlots; ++i) mbar_init(&full[i], 1);
+    fence_mbar_init();
+    const size_t nchunks = (bytes + kTmaChunk - 1) / kTmaChunk;
+    size_t issued = 0, done = 0;
+    // chunk j of this CTA = global chunk blockIdx.x + j * gridDim.x
+    auto chunk_of = [&](size_t j) { return (size_t)blockIdx.x + j * gridDim.x; };
+    size_t mine = nchunks > blockIdx.x ? (nchunks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    while (done < mine) {
+        while (issued < mine && issued - done < (size_t)kTmaSlots) {
+            const int slot = (int)(issued % kTmaSlots);
+            if (issued >= (size_t)kTmaSlots) {
+                // the slot's previous store must have finished reading shared memory
+                asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kTmaSlots - 1) : "memory");
+            }
+            const size_t c = chunk_of(issued);
+            const uint32_t n = (uint32_t)min((size_t)kTmaChunk, bytes - c * kTmaChunk);
+            mbar_expect_tx(&full[slot], n);
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_u32(ring + (size_t)slot * kTmaChunk)),
+                "l"(reinterpret_cast<uint64_t>(src + c * kTmaChunk)), "r"(n), "r"(smem_u32(&full[slot]))
+                : "memory");
+            ++issued;
+        }
+        const int slot = (int)(done % kTmaSlots);
+        mbar_wait(&full[slot], (uint32_t)((done / kTmaSlots) & 1));
+        const size_t c = chunk_of(done);
+        const uint32_t n = (uint32_t)min((size_t)kTmaChunk, bytes - c * kTmaChunk);
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                         reinterpret_cast<uint64_t>(dst + c * kTmaChunk)),
+                     "r"(smem_u32(ring + (size_t)slot * kTmaChunk)), "r"(n)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        ++done;
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+}  // namespace ds_zc
+
+extern "C" int ds_h2d_tma_copy(void* dst, const void* src_host, size_t bytes, int ctas, void* stream) {
+    DS_CHECK_ARG(dst && src_host, "ds_h2d_tma_copy: NULL pointer");
+    DS_CHECK_ARG(bytes % 16 == 0 && ((uintptr_t)dst & 15) == 0 && ((uintptr_t)src_host & 15) == 0,
+                 "ds_h2d_tma_copy: pointers and size must be 16-byte aligned");
+    DS_CHECK_ARG(ctas > 0 && ctas <= 1024, "ds_h2d_tma_copy: ctas=%d", ctas);
+    void* dsrc = nullptr;
+    cudaError_t e = cudaHostGetDevicePointer(&dsrc, const_cast<void*>(src_host), 0);
+    if (e != cudaSuccess) return cuda_status(e, "ds_h2d_tma_copy: source is not mapped pinned host memory");
+    if (bytes == 0) return DS_OK;
+    static bool attr = false;
+    const int smem = ds_zc::kTmaChunk * ds_zc::kTmaSlots;
+    if (!attr) {
+        cudaFuncSetAttribute(ds_zc::tma_copy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
+    }
+    ds_zc::tma_copy_kernel<<<ctas, 32, smem, ds::as_stream(stream)>>>(static_cast<uint8_t*>(dst),
+                                                                      static_cast<const uint8_t*>(dsrc), bytes);
+    DS_LAUNCH_CHECK("ds_h2d_tma_copy");
     return DS_OK;
 }

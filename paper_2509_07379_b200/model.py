@@ -213,3 +213,62 @@ def attention_decode_static(shape: ModelShape, L: dict, h: torch.Tensor, kv: KVC
 
 def logits_last(shape: ModelShape, W: DenseWeights, h_last: torch.Tensor) -> torch.Tensor:
     return (rms_norm(h_last, W.norm, shape.rms_eps) @ W.lm_head).float()
+
+
+# ------------------------------------------------------------- batched serving
+# B sequences of equal prompt length served together (BASELINE config 4:
+# batch 1-32 x prompt 128-2048).  Same numerics as the single-sequence path:
+# the projections take the B*T rows at once (GEMV for <= GEMV_MAX_ROWS rows,
+# else the tcgen05 GEMM), attention runs per sequence inside one SDPA call.
+
+class KVCacheBatch:
+    """[L, B, kv_heads, max_seq, head_dim] bf16 keys / values; every sequence
+    of the batch sits at the same position (equal prompt lengths)."""
+
+    def __init__(self, shape: ModelShape, batch: int, max_seq: int, device):
+        self.k = torch.zeros(shape.num_layers, batch, shape.n_kv_heads, max_seq, shape.head_dim,
+                             dtype=torch.bfloat16, device=device)
+        self.v = torch.zeros_like(self.k)
+        self.len = 0
+
+    @property
+    def nbytes(self) -> int:
+        return self.k.nbytes + self.v.nbytes
+
+
+def attention_block_batch(shape: ModelShape, L: dict, h: torch.Tensor, kv: KVCacheBatch, layer: int, pos0: int,
+                          cos: torch.Tensor, sin: torch.Tensor) -> torch.Tensor:
+    """h [B, T, d] bf16 (positions pos0 .. pos0+T-1 of every sequence) -> h + attn(norm(h))."""
+    B, T, d = h.shape
+    nh, nkv, hd = shape.n_heads, shape.n_kv_heads, shape.head_dim
+    hf = h.reshape(B * T, d)
+    a = rms_norm(hf, L["ln1"], shape.rms_eps)
+    q, k, v = _qkv(shape, L, a)                                  # [B*T, heads, hd]
+    c, s = cos[pos0:pos0 + T].repeat(B, 1), sin[pos0:pos0 + T].repeat(B, 1)
+    q, k = apply_rope(q, c, s), apply_rope(k, c, s)
+    kv.k[layer, :, :, pos0:pos0 + T] = k.view(B, T, nkv, hd).transpose(1, 2)
+    kv.v[layer, :, :, pos0:pos0 + T] = v.view(B, T, nkv, hd).transpose(1, 2)
+    K = kv.k[layer, :, :, :pos0 + T]
+    V = kv.v[layer, :, :, :pos0 + T]
+    o = F.scaled_dot_product_attention(q.view(B, T, nh, hd).transpose(1, 2), K, V,
+                                       is_causal=(T > 1 and pos0 == 0), enable_gqa=True)
+    o = o.transpose(1, 2).reshape(B * T, nh * hd)
+    return _o_proj_residual(L, o, hf).view(B, T, d)
+
+
+def attention_decode_static_batch(shape: ModelShape, L: dict, h: torch.Tensor, kv: KVCacheBatch, layer: int,
+                                  pos: torch.Tensor, mask: torch.Tensor, cos: torch.Tensor,
+                                  sin: torch.Tensor) -> torch.Tensor:
+    """One decode token per sequence with the position on the device (CUDA-graph
+    capturable): h [B, d]; pos int64 [1]; mask [1, 1, 1, max_seq] additive."""
+    B = h.shape[0]
+    nh, nkv, hd = shape.n_heads, shape.n_kv_heads, shape.head_dim
+    a = rms_norm(h, L["ln1"], shape.rms_eps)
+    q, k, v = _qkv(shape, L, a)                                  # [B, heads, hd]
+    c, s = cos.index_select(0, pos).expand(B, -1), sin.index_select(0, pos).expand(B, -1)
+    q, k = apply_rope(q, c, s), apply_rope(k, c, s)
+    kv.k[layer].index_copy_(2, pos, k.unsqueeze(2))             # [B, nkv, 1, hd] at position pos
+    kv.v[layer].index_copy_(2, pos, v.unsqueeze(2))
+    o = F.scaled_dot_product_attention(q.unsqueeze(2), kv.k[layer], kv.v[layer], attn_mask=mask, enable_gqa=True)
+    o = o.squeeze(2).reshape(B, nh * hd)
+    return _o_proj_residual(L, o, h)

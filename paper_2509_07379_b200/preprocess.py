@@ -101,6 +101,9 @@ def preprocess(eng, prompts, decode_len: int, epochs: int = 20, train_fraction: 
         dec = te.filter_phase(DECODE) if hasattr(te, "filter_phase") else None
         if dec is not None and dec.traces:
             held_dec = evaluate(net, dec, pop, aff)
+    # the batched evaluation sized the cached device net's workspace for
+    # thousands of rows; drop it so the serving engine starts from a fresh one
+    net.invalidate_device()
     t3 = time.time()
     return PreprocessResult(net=net, pop=pop, aff=aff, train_report=rep, held_out=held, held_out_decode=held_dec,
                             timings_s={"collect": round(t1 - t0, 2), "train": round(t2 - t1, 2),
