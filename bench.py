@@ -76,6 +76,11 @@ def parse():
                          "shard + cache, NCCL all-reduce combine) on ONE request instead of N replicas")
     ap.add_argument("--ep-combine", default="allreduce", choices=["allreduce", "alltoall"],
                     help="--ep combine collective: one all-reduce, or all_to_all_single + all-gather")
+    ap.add_argument("--sweep", action="store_true",
+                    help="BASELINE config 4: batch x prompt grid through BatchEngine (one JSON document)")
+    ap.add_argument("--sweep-batches", default="1,2,4,8,16,32")
+    ap.add_argument("--sweep-prompts", default="128,256,512,1024,2048")
+    ap.add_argument("--sweep-decode", type=int, default=16)
     ap.add_argument("--out", default=None, help="also write the JSON line to this file")
     return ap.parse_args()
 
@@ -533,8 +538,106 @@ def run_ours(args):
         Path(args.out).write_text(out + "\n")
 
 
+def run_sweep(args):
+    """BASELINE config 4 (Mixtral-8x7B W4, batch 1-32 x prompt 128-2048): per
+    grid point one warm-up and one timed request of B sequences through
+    BatchEngine (prefill B x P, then --sweep-decode decode steps), measured
+    with CUDA events: TTFT, decode ms/step, tokens/s, activated experts per
+    layer (prefill and decode), rows per expert (the K4 GEMV vs tcgen05 GEMM
+    crossover), predictor hit rates, host-link bytes and peak device bytes."""
+    import torch
+    from paper_2509_07379_b200 import _lib
+    from paper_2509_07379_b200.config import load_shape
+    from paper_2509_07379_b200.engine import BatchEngine, Engine
+    _lib.load()
+    dev = torch.device("cuda", 0)
+    shape = load_shape(args.config)
+    batches = [int(x) for x in args.sweep_batches.split(",")]
+    prompts = [int(x) for x in args.sweep_prompts.split(",")]
+    D = args.sweep_decode
+    t0 = time.time()
+    serve_kw = dict(seed=args.seed, device=dev, max_seq=args.prefill + max(args.calib_decode, D) + 8,
+                    max_prefill=args.prefill, cancel_mispredicted=not args.no_cancel, chunk_mb=args.chunk_mb,
+                    link_depth=args.link_depth, spec_chunk_mb=args.spec_chunk_mb)
+    if args.predictor == "trained":
+        pre, dense, store = calibrate(shape, args, serve_kw, None, 0, 1, None)
+        net, pop, aff = pre.net, pre.pop, pre.aff
+    else:
+        net, pop, aff = predictor_inputs(shape)
+        tmp = Engine(shape, "ondemand", **serve_kw)
+        dense, store = tmp.W, tmp.store
+        tmp.close()
+        del tmp
+    points = []
+    for P in prompts:
+        for B in batches:
+            eng = BatchEngine(shape, "duoserve", batch=B, max_prompt=P, max_seq=P + D + 8, dense=dense,
+                              store=store, predictor=net, pop=pop, aff=aff, seed=args.seed, device=dev,
+                              cancel_mispredicted=not args.no_cancel, chunk_mb=args.chunk_mb,
+                              link_depth=args.link_depth, spec_chunk_mb=args.spec_chunk_mb)
+            g = torch.Generator().manual_seed(args.seed + 7 * B + P)
+            ids = torch.randint(0, shape.vocab, (B, P), generator=g).pin_memory()
+            prof = eng.enable_profile()
+            res = None
+            torch.cuda.reset_peak_memory_stats(dev)
+            for it in range(2):                       # warm-up, timed
+                eng.reset()
+                prof.reset()
+                c0 = eng.h2d_bytes()
+                e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+                torch.cuda.synchronize()
+                e0.record()
+                eng.prefill(ids.to(dev, non_blocking=True))
+                e1.record()
+                for _ in range(D):
+                    eng.decode_step()
+                e2.record()
+                torch.cuda.synchronize()
+                res = (e0.elapsed_time(e1), e1.elapsed_time(e2), eng.h2d_bytes() - c0)
+            ttft, dec_ms, h2d = res
+            L = shape.num_layers
+            pre_act = [len(r["activated"]) for r in eng.log if r["phase"] == "prefill"]
+            dec_act = [len(r.get("gate", r.get("fetch", []))) for r in eng.log if r["phase"] == "decode"]
+            rows = [r for _, _, gates in eng._batch_sets for r in gates]
+            kern = prof.summary(measured_peaks())
+            hs = eng.hit_summary()
+            points.append({
+                "batch": B, "prompt": P, "decode_steps": D, "ttft_ms": round(ttft, 2),
+                "decode_ms_per_step": round(dec_ms / D, 3),
+                "decode_tok_s": round(B * D / (dec_ms / 1e3), 2),
+                "prefill_tok_s": round(B * P / (ttft / 1e3), 1),
+                "activated_per_layer": {"prefill": round(sum(pre_act) / max(len(pre_act), 1), 3),
+                                        "decode": round(sum(dec_act) / max(len(dec_act), 1), 3)},
+                "decode_rows_per_expert": round(B * shape.top_k / max(sum(dec_act) / max(len(dec_act), 1), 1e-9), 3),
+                "predictor": {k: hs[k] for k in ("topk_hit_rate", "at_least_one_rate", "prefetch_hits",
+                                                 "prefetch_misses")},
+                "h2d_gb_per_request": round(h2d / 1e9, 3),
+                "peak_device_gb": round(torch.cuda.max_memory_allocated(dev) / 1e9, 3),
+                "kernels": [{k: r[k] for k in ("kernel", "launches", "avg_us", "achieved", "unit", "frac")}
+                            for r in kern["all"]],
+            })
+            print(json.dumps(points[-1]), flush=True)
+            eng.close()
+            del eng
+            torch.cuda.empty_cache()
+    doc = {"metric": "BASELINE config 4 sweep: TTFT / decode tok/s / activated experts / predictor hit rate",
+           "config": {"model": shape.name, "batches": batches, "prompts": prompts, "decode_steps": D,
+                      "policy": "duoserve", "predictor": args.predictor,
+                      "slots": "2 * min(M, k * B) (B = 1: the SPEC's 2k)"},
+           "points": points, "wall_s": round(time.time() - t0, 1),
+           "note": "residency cap applies to the batch-1 metric config; activations and KV of large batches "
+                   "exceed it by construction"}
+    out = json.dumps(doc)
+    print(out)
+    if args.out:
+        Path(args.out).write_text(out + "\n")
+
+
 def main():
     args = parse()
+    if args.sweep:
+        run_sweep(args)
+        return
     if args.impl == "reference":
         run_reference(args)
     else:

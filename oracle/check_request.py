@@ -97,3 +97,39 @@ def check_request(eng_log, paths_prefill, paths_decode, L: int, k: int, net=None
     bad_log = sum(1 for a, b in zip(eng_log, exp) if a != b) + abs(len(exp) - len(eng_log))
     return {"predicted_sets": n_pred, "set_mismatches": bad_pred, "log_records": n_rec, "log_mismatches": bad_log,
             "log_equal": bad_log == 0}
+
+
+def check_request_batch(eng_log, paths_prefill, paths_decode_b, batch_sets, L: int, k: int, net=None,
+                        pop_values=None, aff_values=None, policy: str = "duoserve", pinned=None,
+                        mode: str = "pool") -> dict:
+    """Batched serving (engine.BatchEngine): every sequence's prediction at
+    every decode step and layer >= 1 vs the reference predictor on that
+    sequence's recorded path, and the whole cache log vs sim_ref's batch
+    extension (prefill: the union over all B*P tokens, exactly the
+    single-sequence rule; decode: unions over the batch).
+    paths_decode_b[t][b] = sequence b's path at step t; batch_sets = the
+    engine's (layer, per-sequence predicted sets, per-sequence gate sets)."""
+    T = len(paths_decode_b)
+    B = len(paths_decode_b[0]) if T else 0
+    preds_b = [[None] * B for _ in range(T)]
+    n_pred = bad_pred = 0
+    if policy == "duoserve" and T:
+        for b in range(B):
+            pb = predictions(net, [paths_decode_b[t][b] for t in range(T)], L, pop_values, aff_values, k, mode)
+            for t in range(T):
+                preds_b[t][b] = pb[t]
+        want = [(t, l) for t in range(T) for l in range(1, L)]
+        n_pred = len(want) * B
+        for (layer, sets, _), (t, l) in zip(batch_sets, want):
+            for b in range(B):
+                if layer != l or tuple(sets[b]) != tuple(sorted(preds_b[t][b][l])):
+                    bad_pred += 1
+        bad_pred += abs(len(batch_sets) - len(want)) * B
+    pre = [tuple(tuple(int(e) for e in paths_prefill[t, l]) for l in range(L)) for t in range(paths_prefill.shape[0])]
+    pins = set(pinned) if pinned else None
+    exp = (sim_ref.cache_log_prefill(pre, L, policy, pinned=pins)
+           + sim_ref.cache_log_decode_batch(paths_decode_b, preds_b, L, policy, pinned=pins)[0])
+    n_rec = max(len(exp), len(eng_log))
+    bad_log = sum(1 for a, b in zip(eng_log, exp) if a != b) + abs(len(exp) - len(eng_log))
+    return {"predicted_sets": n_pred, "set_mismatches": bad_pred, "log_records": n_rec, "log_mismatches": bad_log,
+            "log_equal": bad_log == 0}

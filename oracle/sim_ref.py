@@ -101,6 +101,36 @@ def cache_log_decode(paths, preds, L: int, policy: str = "duoserve", owned=None,
     return log, {"prefetch_hits": hits, "prefetch_misses": misses, "refetch_count": refetches}
 
 
+def cache_log_decode_batch(paths_b, preds_b, L: int, policy: str = "duoserve", pinned=None):
+    """Batch extension of cache_log_decode (a build extension: the SPEC's
+    simulator excludes batching).  paths_b[t][b][l] = gate
+    selection of sequence b at decode step t, layer l; preds_b[t][b][l] =
+    its predicted set (l >= 1).  Per (t, l) the activated set is the union of
+    the B selections and the predicted set the union of the B predictions;
+    the record is then formed exactly as for one sequence:
+      l = 0 (or ondemand): fetch the union (minus pinned experts);
+      l >= 1: pred = union of predictions, gate = union of selections,
+              refetch = gate minus pinned minus pred."""
+    log = []
+    hits = misses = 0
+    for t, step in enumerate(paths_b):
+        for l in range(L):
+            A = _sorted({e for path in step for e in path[l]})
+            pins = {e for (ll, e) in (pinned or ()) if ll == l}
+            extra = {"pinned": _sorted(set(A) & pins)} if pinned else {}
+            if l == 0 or policy == "ondemand":
+                log.append({"phase": "decode", "token": t, "layer": l, "fetch": [e for e in A if e not in pins],
+                            "kind": "ondemand", **extra})
+                continue
+            P = _sorted({e for pr in preds_b[t] for e in pr[l]})
+            Ed = set(A) - pins
+            miss = _sorted(Ed - set(P))
+            hits += len(Ed & set(P))
+            misses += len(miss)
+            log.append({"phase": "decode", "token": t, "layer": l, "pred": P, "gate": A, "refetch": miss, **extra})
+    return log, {"prefetch_hits": hits, "prefetch_misses": misses}
+
+
 # --------------------------------------------------------------------------
 # integer-ns timelines for the SPEC fixtures
 

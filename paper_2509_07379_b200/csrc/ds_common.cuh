@@ -38,7 +38,10 @@ int num_sms();
 // until gate_release() — issued after every launch of the span is queued —
 // so the span covers device execution only.  Returns 0 when the stream memory
 // operations are unavailable (then the span is recorded ungated).
-// DS_LAUNCH_GATE=0 disables it (A/B runs).
+// Between hold and release the caller must not make a synchronous CUDA call
+// (cudaMemcpy, cudaMemset, cudaMalloc, ...): on the legacy default stream it
+// would wait for the held work and never return.  DS_LAUNCH_GATE=0 disables
+// the gate (A/B runs).
 unsigned gate_hold(cudaStream_t st);
 void gate_release(unsigned seq);
 

@@ -29,6 +29,8 @@ GateState* gate_state() {
     std::call_once(g_gate_once[dev], [dev] {
         const char* env = getenv("DS_LAUNCH_GATE");
         if (env && env[0] == '0') return;
+        // the diagnostic K4 paths allocate / synchronise inside the launch call
+        if (getenv("DS_K4_TIMELINE") || (getenv("DS_K4_FUSED") && getenv("DS_K4_FUSED")[0] == '1')) return;
         void* p = nullptr;
         if (cudaGetSymbolAddress(&p, g_launch_gate) != cudaSuccess) { cudaGetLastError(); return; }
         cudaStream_t rs = nullptr;
@@ -60,7 +62,14 @@ unsigned gate_hold(cudaStream_t st) {
 void gate_release(unsigned seq) {
     if (!seq) return;
     GateState* g = gate_state();
-    if (g && g->ok) cuStreamWriteValue32((CUstream)g->release, g->word, seq, CU_STREAM_WRITE_VALUE_DEFAULT);
+    if (g && g->ok &&
+        cuStreamWriteValue32((CUstream)g->release, g->word, seq, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS) {
+        // never leave a stream held: fall back to an ordinary async copy of the value
+        static thread_local unsigned v;
+        v = seq;
+        cudaMemcpyAsync((void*)g->word, &v, sizeof(v), cudaMemcpyHostToDevice, g->release);
+        cudaStreamSynchronize(g->release);
+    }
 }
 
 static thread_local char g_err[512] = "";

@@ -302,10 +302,7 @@ struct Geo {
 }  // namespace k4s
 
 __device__ unsigned g_k4s_ticket[k4s::kTicketSlots];
-// L2 run-ahead of the bulk-staged GEMV producers: with block t in flight to
-// shared memory, block t + g_k4s_ahead is prefetched into L2, so the block's
-// bulk copy later hits L2 (0 = off; DS_K4S_L2AHEAD, set once per process)
-__device__ int g_k4s_ahead;
+
 __device__ unsigned g_k4s_done[k4s::kTicketSlots];
 
 // stage_x for the consumer warps only (named barrier 1): all loads of a
@@ -350,18 +347,6 @@ __device__ __forceinline__ void k4s_produce(const W4Ptr (&W)[2], int N, int S, i
     const int T = (N + RB - 1) / RB;
     unsigned* tk = g_k4s_ticket + slot_id;
     const uint64_t pol = l2_evict_first_policy();
-    const int ahead = g_k4s_ahead;
-    if (ahead > 0) {                                       // the run-ahead window starts with this CTA's first grab
-        const int b0 = (int)blockIdx.x * S;
-        for (int j = 0; j < S && b0 + j + ahead < T; ++j) {
-            const int ra = (b0 + j + ahead) * RB;
-            if (ra >= N) break;
-#pragma unroll
-            for (int m = 0; m < NMAT; ++m)
-                bulk_prefetch_l2(reinterpret_cast<const uint8_t*>(W[m].codes) + (size_t)ra * Gm::CODE_B,
-                                 min(RB, N - ra) * Gm::CODE_B);
-        }
-    }
     const int first = (int)atomicAdd(tk, (unsigned)S);   // the first S blocks in one grab
     int pending = -1;
     int sentinels = 0;
@@ -383,17 +368,6 @@ __device__ __forceinline__ void k4s_produce(const W4Ptr (&W)[2], int N, int S, i
         const uint32_t zb1 = (((uint32_t)((r0 + rows) * GPR) >> 1) + 15u) & ~15u;
         const uint32_t cb = rows * Gm::CODE_B, sb = rows * Gm::SC_B, zb = zb1 - zb0;
         mbar_expect_tx(&full[slot], NMAT * (cb + sb + zb));
-        const int ta = t + ahead;
-        if (ahead > 0 && ta < T) {
-            const int ra = ta * RB, rowsa = min(RB, N - ra);
-#pragma unroll
-            for (int m = 0; m < NMAT; ++m) {
-                bulk_prefetch_l2(reinterpret_cast<const uint8_t*>(W[m].codes) + (size_t)ra * Gm::CODE_B,
-                                 rowsa * Gm::CODE_B);
-                bulk_prefetch_l2(reinterpret_cast<const uint8_t*>(W[m].scales) + (size_t)ra * Gm::SC_B,
-                                 rowsa * Gm::SC_B);
-            }
-        }
 #pragma unroll
         for (int m = 0; m < NMAT; ++m) {
             uint8_t* md = dst + m * Gm::MAT_B;
@@ -1032,19 +1006,7 @@ static int down_launch_u(const __nv_bfloat16* h, const ds_w4_expert* e, int d, i
 // the older variants (A/B runs).
 // one ticket slot per launch, shared by every instantiation (a SwiGLU GEMV and
 // the PDL down GEMV that overlaps it must not share a counter)
-inline void k4s_set_ahead_once() {
-    static thread_local int done_dev = -1;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (done_dev == dev) return;
-    const char* env = getenv("DS_K4S_L2AHEAD");
-    int v = env ? atoi(env) : 0;
-    cudaMemcpyToSymbol(g_k4s_ahead, &v, sizeof(int));
-    done_dev = dev;
-}
-
 inline unsigned k4s_next_slot() {
-    k4s_set_ahead_once();
     static std::atomic<unsigned> seq{0};
     return seq.fetch_add(1, std::memory_order_relaxed) % k4s::kTicketSlots;
 }

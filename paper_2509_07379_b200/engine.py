@@ -43,8 +43,9 @@ import torch
 
 from . import ops
 from .config import ModelShape, SchedulerPolicy, model_config_for_shape, slot_count
-from .model import (DenseWeights, KVCache, attention_block, attention_decode_static, init_dense_weights,
-                    logits_last, rms_norm, rope_tables)
+from .model import (DenseWeights, KVCache, KVCacheBatch, attention_block, attention_block_batch,
+                    attention_decode_static, attention_decode_static_batch, init_dense_weights, logits_last,
+                    rms_norm, rope_tables)
 from .ep import EPConfig, owned_experts, owner_mask
 from .predictor import ExpertMLP, StatsOnDevice, _mode_code
 from .stats import OnlineRoutingStats
@@ -345,18 +346,18 @@ class LinkQueue:
 class MLPDriver:
     """K5 on the predict stream: P_{l+1} from the device history buffer."""
 
-    def __init__(self, net: ExpertMLP, pop, aff, L: int, M: int, k: int, device):
+    def __init__(self, net: ExpertMLP, pop, aff, L: int, M: int, k: int, device, batch: int = 1):
         self.dev = net.device(device)
         self.stats = StatsOnDevice(pop, aff, device)
         self.mode = _mode_code(net.meta.get("affinity_mode", "pool"))
-        self.L, self.M, self.k = L, M, k
+        self.L, self.M, self.k, self.B = L, M, k, batch
         self.stream = torch.cuda.Stream(device)
-        self.target = torch.zeros(1, dtype=torch.int32, device=device)
-        self.targets = [torch.full((1,), l, dtype=torch.int32, device=device) for l in range(L)]
-        self.out = torch.empty((1, k), dtype=torch.int32, device=device)
-        self.probs = torch.empty((1, M), dtype=torch.float64, device=device)
-        self.host_out = torch.empty((1, k), dtype=torch.int32, pin_memory=True)
-        self.host_probs = torch.empty((1, M), dtype=torch.float64, pin_memory=True)
+        self.targets = [torch.full((batch,), l, dtype=torch.int32, device=device) for l in range(L)]
+        self.out = torch.empty((batch, k), dtype=torch.int32, device=device)
+        self.probs = torch.empty((batch, M), dtype=torch.float64, device=device)
+        self.host_out = torch.empty((batch, k), dtype=torch.int32, pin_memory=True)
+        self.host_probs = torch.empty((batch, M), dtype=torch.float64, pin_memory=True)
+        self.sets = None                 # per-sequence predicted sets of the last result()
         self.done = torch.cuda.Event()
         self.nbytes = self.dev.nbytes + self.stats.pop.nbytes + self.stats.aff.nbytes
 
@@ -371,13 +372,22 @@ class MLPDriver:
             self.done.record(self.stream)
 
     def result(self, link=None) -> tuple:
-        """(sorted predicted set, transfer order = descending probability)."""
+        """(sorted predicted set, transfer order = descending probability).
+        With B sequences: the union of their sets, ordered by descending
+        probability summed over the batch (ties: lower index); for B = 1 that
+        is the single sequence's order."""
         if link is not None:
             link.wait_event(self.done)
         self.done.synchronize()
-        P = [int(e) for e in self.host_out[0].tolist()]
-        pr = self.host_probs[0].tolist()
-        return P, sorted(P, key=lambda e: (-pr[e], e))
+        rows = self.host_out.tolist()
+        self.sets = [tuple(sorted(int(e) for e in r)) for r in rows]
+        if self.B == 1:
+            P = [int(e) for e in rows[0]]
+            pr = self.host_probs[0].tolist()
+            return P, sorted(P, key=lambda e: (-pr[e], e))
+        P = sorted({e for r in self.sets for e in r})
+        score = self.host_probs.sum(dim=0).tolist()
+        return P, sorted(P, key=lambda e: (-score[e], e))
 
 
 class TraceDriver:
@@ -425,20 +435,21 @@ class Engine:
         self.owned_set = set(self.owned)
         self.store = store if store is not None else HostExpertStore(sh, seed, self.device, experts=self.owned)
         cfg = model_config_for_shape(sh)
-        self.n_slots = slot_count(self.policy, cfg)
+        self.B = getattr(self, "B", 1)           # sequences served together (BatchEngine sets B first)
+        self.n_slots = self._slot_count(cfg)
         self.cache = ExpertCache(self.store, self.n_slots, self.device)
         self.cancel_mispredicted = cancel_mispredicted
         self.link = LinkQueue(self.cache, int(chunk_mb * 2**20) if cancel_mispredicted else 0,
                               link_depth if cancel_mispredicted else 2, cancel_mispredicted,
                               spec_chunk_bytes=int(spec_chunk_mb * 2**20))
         self.max_seq, self.max_prefill = int(max_seq), int(max_prefill)
-        self.kv = KVCache(sh, max_seq, self.device)
+        self.kv = self._make_kv(max_seq)
         self.cos, self.sin = rope_tables(sh, max_seq, self.device)
         self.driver = None
         if self.policy is SchedulerPolicy.DUOSERVE:
             if predictor is None or pop is None or aff is None:
                 raise ValueError("policy 'duoserve' needs predictor, pop and aff")
-            self.driver = MLPDriver(predictor, pop, aff, self.L, self.M, self.k, self.device)
+            self.driver = MLPDriver(predictor, pop, aff, self.L, self.M, self.k, self.device, batch=self.B)
         elif self.policy is SchedulerPolicy.DUOSERVE_ORACLE:
             if oracle_paths is None:
                 raise ValueError("policy 'oracle' needs the recorded decode routing (oracle_paths)")
@@ -450,11 +461,12 @@ class Engine:
         self._pinned_buf = None
         if pin_budget_bytes > 0:
             self.pin_experts(pop, int(pin_budget_bytes))
-        # decode buffers
-        self.hist = torch.zeros((1, self.L * self.k), dtype=torch.int32, device=dev)
-        self.idx1 = torch.empty((1, self.k), dtype=torch.int32, device=dev)
-        self.w1 = torch.empty((1, self.k), dtype=torch.float32, device=dev)
-        self.idx_host = torch.empty((1, self.k), dtype=torch.int32, pin_memory=True)
+        # decode buffers (one row per sequence)
+        B = self.B
+        self.hist = torch.zeros((B, self.L * self.k), dtype=torch.int32, device=dev)
+        self.idx1 = torch.empty((B, self.k), dtype=torch.int32, device=dev)
+        self.w1 = torch.empty((B, self.k), dtype=torch.float32, device=dev)
+        self.idx_host = torch.empty((B, self.k), dtype=torch.int32, pin_memory=True)
         self.h_buf = torch.empty((1, self.ff), dtype=torch.bfloat16, device=dev)
         self.acc = torch.zeros((1, self.d), dtype=torch.float32, device=dev)
         self.ev_gate = torch.cuda.Event()
@@ -517,6 +529,12 @@ class Engine:
         if not self.pinned:
             return list(experts), []
         return [e for e in experts if (l, e) not in self.pinned], [e for e in experts if (l, e) in self.pinned]
+
+    def _slot_count(self, cfg) -> int:
+        return slot_count(self.policy, cfg)
+
+    def _make_kv(self, max_seq: int):
+        return KVCache(self.shape, max_seq, self.device)
 
     # ------------------------------------------------------------------ API
     def reset(self) -> None:
@@ -627,10 +645,13 @@ class Engine:
         self.t_decode += 1
         return tok
 
+    def _attn_decode(self, l: int):
+        return attention_decode_static(self.shape, self.W.layers[l], self.g_h, self.kv, l, self.g_pos, self.g_mask,
+                                       self.cos, self.sin)
+
     def _decode_layer_front(self, l: int) -> None:
         """attention(l) + rms_norm + K1 gate on static buffers (captured per layer)."""
-        h1 = attention_decode_static(self.shape, self.W.layers[l], self.g_h, self.kv, l, self.g_pos, self.g_mask,
-                                     self.cos, self.sin)
+        h1 = self._attn_decode(l)
         self.g_h1.copy_(h1)
         self.g_a2.copy_(rms_norm(h1, self.W.layers[l]["ln2"], self.shape.rms_eps))
         ops.gate_topk(self.g_a2, self.W.layers[l]["wg"], self.k, self.idx1, self.w1, hist=self.hist, layer=l)
@@ -639,14 +660,15 @@ class Engine:
         if self.g_graphs is not None:
             return
         dev, d = self.device, self.d
-        max_seq = self.kv.k.shape[2]
+        max_seq = self.kv.k.shape[-2]
+        B = self.B
         self.g_pos = torch.zeros(1, dtype=torch.long, device=dev)
-        self.g_tok = torch.zeros(1, dtype=torch.long, device=dev)
+        self.g_tok = torch.zeros(B, dtype=torch.long, device=dev)
         self.g_ar = torch.arange(max_seq, device=dev)
         self.g_mask = torch.zeros((1, 1, 1, max_seq), dtype=torch.bfloat16, device=dev)
-        self.g_h = torch.zeros((1, d), dtype=torch.bfloat16, device=dev)
-        self.g_h1 = torch.zeros((1, d), dtype=torch.bfloat16, device=dev)
-        self.g_a2 = torch.zeros((1, d), dtype=torch.bfloat16, device=dev)
+        self.g_h = torch.zeros((B, d), dtype=torch.bfloat16, device=dev)
+        self.g_h1 = torch.zeros((B, d), dtype=torch.bfloat16, device=dev)
+        self.g_a2 = torch.zeros((B, d), dtype=torch.bfloat16, device=dev)
         kv_k, kv_v = self.kv.k.clone(), self.kv.v.clone()
         hist = self.hist.clone()
         side = torch.cuda.Stream(dev)
@@ -994,6 +1016,251 @@ class Engine:
         if self._pinned_buf is not None:
             out["pinned_experts"] = self._pinned_buf.numel()
         return out
+
+
+class BatchEngine(Engine):
+    """B sequences of equal prompt length served together (BASELINE config 4:
+    batch 1-32 x prompt 128-2048, the dense-prefill vs sparse-decode
+    crossover).  A build extension — the reference's simulator excludes
+    batching; its cache semantics are extended to the batch's
+    union of selections (oracle/sim_ref.cache_log_decode_batch):
+
+      prefill   the B*P tokens are routed together: A_l = the union over the
+                batch, fetched once per layer exactly as for one sequence;
+      decode    per layer the activated set A_l = the union of the B gate
+                selections; for l >= 1 the predicted set P_l = the union of
+                the B predictions (K5 on B rows), prefetched during layer l-1
+                in order of probability summed over the batch; sync point 1
+                re-fetches A_l minus P_l; the expert rows are grouped by the
+                permute kernel (K2) and each expert runs the K4 GEMV on its
+                rows (<= 16) or the tcgen05 GEMM (K3) above that;
+      capacity  2 * min(M, k*B) slots (duoserve/oracle: one bank for the
+                layer's working set, one for the next layer's prefetch;
+                ondemand: min(M, k*B)); B = 1 gives the SPEC's 2k / k.
+
+    The API mirrors Engine: prefill(ids [B, P]) -> B first tokens,
+    decode_step() -> B tokens; paths_decode[t][b] is sequence b's path."""
+
+    GEMV_ROWS = 16          # K4 up to this many rows per expert, K3 (tcgen05) above
+
+    def __init__(self, shape: ModelShape, policy="duoserve", batch: int = 1, max_prompt: int = 512,
+                 max_seq: int = 2048, **kw):
+        if batch < 1:
+            raise ValueError("batch must be >= 1")
+        if SchedulerPolicy(policy) in (SchedulerPolicy.DUOSERVE_ORACLE, SchedulerPolicy.PREFETCH_ALL):
+            raise ValueError(f"BatchEngine serves 'duoserve' and 'ondemand' (got {policy!r})")
+        if kw.get("ep") is not None:
+            raise ValueError("BatchEngine: expert parallelism is single-sequence only")
+        self.B = int(batch)
+        self.max_prompt = int(max_prompt)
+        super().__init__(shape, policy, max_seq=max_seq, max_prefill=self.B * self.max_prompt, **kw)
+        dev, B, k, d, ff = self.device, self.B, self.k, self.d, self.ff
+        self.d_off = torch.empty(self.M + 1, dtype=torch.int32, device=dev)
+        self.d_off_host = torch.empty(self.M + 1, dtype=torch.int32, pin_memory=True)
+        self.d_pos = torch.empty(B * k, dtype=torch.int32, device=dev)
+        self.d_src = torch.empty(B * k, dtype=torch.int32, device=dev)
+        self.d_xperm = torch.empty((B * k, d), dtype=torch.bfloat16, device=dev)
+        self.d_y = torch.zeros((B * k, d), dtype=torch.float32, device=dev)
+        self.d_h = torch.empty((B * k, ff), dtype=torch.bfloat16, device=dev)
+        self.ones = torch.ones(1, dtype=torch.float32, device=dev)
+        self.d_ws = torch.empty(max(ops.grouped_ffn_workspace(B * k, d, ff), 256), dtype=torch.uint8, device=dev)
+        self.tokens = None
+
+    def _slot_count(self, cfg) -> int:
+        cap = min(self.M, self.k * self.B)
+        if self.policy is SchedulerPolicy.ON_DEMAND:
+            return cap
+        return 2 * cap
+
+    def _make_kv(self, max_seq: int):
+        return KVCacheBatch(self.shape, self.B, max_seq, self.device)
+
+    def _attn_decode(self, l: int):
+        return attention_decode_static_batch(self.shape, self.W.layers[l], self.g_h, self.kv, l, self.g_pos,
+                                             self.g_mask, self.cos, self.sin)
+
+    @torch.no_grad()
+    def prefill(self, ids) -> list:
+        """Prompt pass of the B sequences (ids [B, P]); returns their first tokens."""
+        ids = torch.as_tensor(ids, dtype=torch.long, device=self.device)
+        if ids.dim() != 2 or ids.shape[0] != self.B:
+            raise ValueError(f"prefill needs ids of shape [{self.B}, P], got {tuple(ids.shape)}")
+        P = ids.shape[1]
+        T = self.B * P
+        if P < 1:
+            raise ValueError("prefill needs at least one prompt token")
+        if P > self.max_prompt or P > self.max_seq:
+            raise ValueError(f"prompt of {P} tokens exceeds max_prompt={self.max_prompt} / max_seq={self.max_seq}")
+        h = self.W.embed[ids]                                     # [B, P, d]
+        idx_all = []
+        self._spec_fetch(0)
+        for l in range(self.L):
+            h = attention_block_batch(self.shape, self.W.layers[l], h, self.kv, l, 0, self.cos, self.sin)
+            hf, idx_host = self._moe_prefill(l, h.reshape(T, self.d), T)
+            h = hf.view(self.B, P, self.d)
+            idx_all.append(idx_host)
+        self.kv.len = P
+        self.paths_prefill = np.stack(idx_all, axis=1)           # [B*P, L, k], sequence-major
+        if self.route_stats is not None:
+            self.route_stats.add(self.p_paths[:T])
+        lg = logits_last(self.shape, self.W, h[:, -1])
+        self.last_logits = lg
+        toks = [int(t) for t in torch.argmax(lg, dim=-1).tolist()]
+        self.tokens = toks
+        self.token = toks[0]
+        self.t_decode = 0
+        return toks
+
+    @torch.no_grad()
+    def decode_step(self) -> list:
+        """One greedy token for each of the B sequences."""
+        if self.tokens is None:
+            raise ValueError("decode_step before prefill")
+        pos = self.kv.len
+        if pos + 1 > self.max_seq:
+            raise ValueError(f"decode position {pos} would exceed max_seq={self.max_seq}")
+        self._ensure_decode_graphs()
+        self.g_pos.fill_(pos)
+        self.g_mask.copy_(torch.where(self.g_ar <= pos, 0.0, float("-inf")).view_as(self.g_mask))
+        self.g_tok.copy_(torch.as_tensor(self.tokens, dtype=torch.long), non_blocking=True)
+        self.g_h.copy_(self.W.embed.index_select(0, self.g_tok))
+        paths = [[] for _ in range(self.B)]
+        self._pred_next = None
+        h = self.g_h
+        for l in range(self.L):
+            self.g_graphs[l].replay()                              # attention + norm + K1 gate (B rows)
+            ops._count("ds_gate_topk")
+            h, rows = self._moe_decode_batch(l, self.g_h1, self.g_a2, self.g_h)
+            for b in range(self.B):
+                paths[b].append(rows[b])
+        self.kv.len = pos + 1
+        self.paths_decode.append(tuple(tuple(p) for p in paths))
+        if self.route_stats is not None:
+            self.route_stats.add((self.hist.view(self.B, self.L, self.k) - 1).to(torch.int32))
+        lg = logits_last(self.shape, self.W, h)
+        self.last_logits = lg
+        toks = [int(t) for t in torch.argmax(lg, dim=-1).tolist()]
+        self.tokens = toks
+        self.t_decode += 1
+        return toks
+
+    def generate(self, ids, n_new: int) -> list:
+        """[n_new][B] tokens."""
+        out = [self.prefill(ids)]
+        for _ in range(n_new - 1):
+            out.append(self.decode_step())
+        return out
+
+    def _batch_ffn(self, e: int, off, st) -> None:
+        lo, hi = off[e], off[e + 1]
+        R = hi - lo
+        prof = self.prof
+        evs = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) if prof else (None, None)
+        if R <= self.GEMV_ROWS:
+            ops.expert_gemv(self.d_xperm[lo:hi], st, self.d, self.ff, self.G, self.d_h[:R], self.ones, 0,
+                            self.d_y[lo:hi], *evs)
+            if prof:
+                prof.add("K4 w4_swiglu_gemv+down_gemv", evs[0], evs[1], self.store.blob_bytes)
+        else:
+            ops.grouped_ffn(self.d_xperm[lo:hi], [0, R], [st], self.d, self.ff, self.G, self.d_h[lo:hi],
+                            self.d_y[lo:hi], self.d_ws, *evs)
+            if prof:
+                prof.add("K3 w4_grouped_ffn (tcgen05)", evs[0], evs[1], self.store.blob_bytes,
+                         6.0 * R * self.d * self.ff)
+
+    def _moe_decode_batch(self, l: int, h, a, out):
+        link = self.link
+        B, k, M = self.B, self.k, self.M
+        ops.permute(self.idx1, a, M, self.d_off, self.d_pos, self.d_src, self.d_xperm)
+        self.ev_gate.record()
+        self.idx_host.copy_(self.idx1, non_blocking=True)
+        self.d_off_host.copy_(self.d_off, non_blocking=True)
+        ev_idx = torch.cuda.Event()
+        ev_idx.record()
+        use_pred = self.driver is not None
+        if use_pred and l + 1 < self.L:
+            self.driver.launch(self.hist, self.ev_gate, l + 1)    # predict stream, overlapped
+        link.wait_event(ev_idx)                                    # sync point 1: the batch's selections on the host
+        self.d2h_bytes += self.idx_host.nbytes + self.d_off_host.nbytes + \
+            ((4 * k + 8 * M) * B if use_pred else 0)
+        off = self.d_off_host.tolist()
+        rows = [tuple(int(e) for e in r) for r in self.idx_host.tolist()]
+        if self.capture is not None:
+            self.capture.append(("decode", l, a.cpu(), self.idx_host.clone()))
+        A = [e for e in range(M) if off[e + 1] > off[e]]
+        mine, mine_pin = self._split_pinned(l, A)
+        slot_of, trs, miss = {}, {}, []
+        cap = min(M, k * B)
+        if l == 0 or not use_pred:
+            base = 0 if (l % 2 == 0 or self.n_slots < 2 * cap) else cap
+            for j, e in enumerate(mine):
+                slot = (base + j) % self.n_slots
+                trs[e] = link.submit(slot, l, e)
+                slot_of[e] = slot
+            self.log.append({"phase": "decode", "token": self.t_decode, "layer": l, "fetch": mine,
+                             "kind": "ondemand", **({"pinned": sorted(mine_pin)} if self.pinned else {})})
+        else:
+            P, order, pending = self._pred_next
+            miss = sorted(set(mine) - set(P))
+            spare = [pending[p][0] for p in order if p in pending and p not in A]
+            for p in order:
+                if p not in pending:
+                    continue
+                if p in A:
+                    slot_of[p], trs[p] = pending[p]
+                    link.promote(trs[p])
+                else:
+                    link.cancel(pending[p][1])
+            used = set(slot_of.values())
+            spare += [s_ for s_ in range(self.n_slots) if s_ not in used and s_ not in spare]
+            for e, s_ in zip(miss, spare):
+                trs[e] = link.submit(s_, l, e)
+                slot_of[e] = s_
+            self.log.append({"phase": "decode", "token": self.t_decode, "layer": l, "pred": sorted(P),
+                             "gate": A, "refetch": miss, **({"pinned": sorted(mine_pin)} if self.pinned else {})})
+            self._batch_sets.append((l, self._pred_sets, rows))
+        self.d_y[:B * k].zero_()
+        for e in mine_pin:
+            self._batch_ffn(e, off, self.pinned[(l, e)])
+        for e in [x for x in mine if x not in miss] + miss:
+            link.flush(trs[e])
+            self._batch_ffn(e, off, self.cache.acquire(slot_of[e]))
+            self.cache.release(slot_of[e])
+        ops.unpermute_combine(self.d_y[:B * k], self.d_pos[:B * k], self.w1, h, out)
+        self._record_moe("decode", l, h, a, out, self.idx_host, self.w1)
+        if use_pred and l + 1 < self.L:                            # sync point 2
+            Pn, order = self.driver.result(link)
+            self._pred_sets = list(self.driver.sets)
+            cur = set(slot_of.values())
+            free = [s_ for s_ in range(self.n_slots) if s_ not in cur]
+            pending = {}
+            for e, s_ in zip([e for e in order if (l + 1, e) not in self.pinned], free):
+                pending[e] = (s_, link.submit(s_, l + 1, e, speculative=True))
+            self._pred_next = (Pn, order, pending)
+        return out, rows
+
+    def reset(self) -> None:
+        super().reset()
+        self.tokens = None
+        self._pred_sets = None
+        self._batch_sets = []          # (layer, per-sequence predicted sets, per-sequence gate sets)
+
+    def hit_summary(self) -> dict:
+        """Per-sequence prediction counters (top-k exact / at least one) and
+        the union-level prefetch hits / misses of the cache log."""
+        dec = [r for r in self.log if r["phase"] == "decode" and "pred" in r]
+        hits = sum(len(set(r["pred"]) & set(r["gate"])) for r in dec)
+        miss = sum(len(r["refetch"]) for r in dec)
+        n = exact = any_ = 0
+        for _, preds, gates in self._batch_sets:
+            for p, g in zip(preds, gates):
+                n += 1
+                exact += set(p) == set(g)
+                any_ += bool(set(p) & set(g))
+        return {"policy": self.policy.value, "batch": self.B, **self.link.stats(),
+                "prefetch_hits": hits, "prefetch_misses": miss,
+                "topk_hit_rate": round(exact / n, 4) if n else None,
+                "at_least_one_rate": round(any_ / n, 4) if n else None}
 
 
 def _union(iv: list) -> list:
