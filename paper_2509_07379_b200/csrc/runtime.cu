@@ -14,10 +14,16 @@ namespace ds {
 __device__ unsigned g_launch_gate;       // monotonic: a held stream waits for gate >= its sequence number
 
 namespace {
+// driver entry points resolved at run time (the library links only the CUDA
+// runtime, so it also loads on a machine without a driver)
+typedef CUresult (*WaitValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*WriteValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 struct GateState {
     bool ok = false;
     CUdeviceptr word = 0;
     cudaStream_t release = nullptr;
+    WaitValue32Fn wait = nullptr;
+    WriteValue32Fn write = nullptr;
 };
 GateState g_gate[16];
 std::once_flag g_gate_once[16];
@@ -31,17 +37,30 @@ GateState* gate_state() {
         if (env && env[0] == '0') return;
         // the diagnostic K4 paths allocate / synchronise inside the launch call
         if (getenv("DS_K4_TIMELINE") || (getenv("DS_K4_FUSED") && getenv("DS_K4_FUSED")[0] == '1')) return;
+        void* wf = nullptr;
+        void* rf = nullptr;
+        cudaDriverEntryPointQueryResult q1, q2;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &wf, cudaEnableDefault, &q1) != cudaSuccess ||
+            cudaGetDriverEntryPoint("cuStreamWriteValue32", &rf, cudaEnableDefault, &q2) != cudaSuccess || !wf ||
+            !rf || q1 != cudaDriverEntryPointSuccess || q2 != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            return;
+        }
+        auto wait = reinterpret_cast<WaitValue32Fn>(wf);
+        auto write = reinterpret_cast<WriteValue32Fn>(rf);
         void* p = nullptr;
         if (cudaGetSymbolAddress(&p, g_launch_gate) != cudaSuccess) { cudaGetLastError(); return; }
         cudaStream_t rs = nullptr;
         if (cudaStreamCreateWithFlags(&rs, cudaStreamNonBlocking) != cudaSuccess) { cudaGetLastError(); return; }
         // probe: a wait that is already satisfied (gate >= 0) must be accepted
-        if (cuStreamWaitValue32((CUstream)rs, (CUdeviceptr)p, 0, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS ||
-            cuStreamWriteValue32((CUstream)rs, (CUdeviceptr)p, 0, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS ||
+        if (wait((CUstream)rs, (CUdeviceptr)p, 0, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS ||
+            write((CUstream)rs, (CUdeviceptr)p, 0, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS ||
             cudaStreamSynchronize(rs) != cudaSuccess) {
             cudaGetLastError();
             return;
         }
+        g_gate[dev].wait = wait;
+        g_gate[dev].write = write;
         g_gate[dev].word = (CUdeviceptr)p;
         g_gate[dev].release = rs;
         g_gate[dev].ok = true;
@@ -55,7 +74,7 @@ unsigned gate_hold(cudaStream_t st) {
     if (!g || !g->ok) return 0;
     unsigned seq = g_gate_seq.fetch_add(1, std::memory_order_relaxed) + 1;
     if (seq == 0) seq = g_gate_seq.fetch_add(1, std::memory_order_relaxed) + 1;     // 0 means "not held"
-    if (cuStreamWaitValue32((CUstream)st, g->word, seq, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS) return 0;
+    if (g->wait((CUstream)st, g->word, seq, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS) return 0;
     return seq;
 }
 
@@ -63,7 +82,7 @@ void gate_release(unsigned seq) {
     if (!seq) return;
     GateState* g = gate_state();
     if (g && g->ok &&
-        cuStreamWriteValue32((CUstream)g->release, g->word, seq, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS) {
+        g->write((CUstream)g->release, g->word, seq, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS) {
         // never leave a stream held: fall back to an ordinary async copy of the value
         static thread_local unsigned v;
         v = seq;
