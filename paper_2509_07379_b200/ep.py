@@ -126,3 +126,90 @@ class EPConfig:
 
     def owns(self, expert: int) -> bool:
         return owner(expert, self.world) == self.rank
+
+
+# ---------------------------------------------------------------------------
+# Token dispatch / combine over all-to-all ("NCCL all-to-all
+# dispatch of permuted rows ... plus an all-to-all combine").  For batch > 1
+# the tokens are partitioned over the ranks (each rank owns some sequences,
+# their attention and KV cache) and the experts are sharded by `owner`:
+#
+#   1. every rank groups its (token, slot) rows by destination rank (the
+#      owner of the selected expert), stable in (expert, token, slot) order;
+#   2. all_to_all_single exchanges the row counts, then the bf16 rows and
+#      their expert ids (variable splits);
+#   3. each owner runs its experts on the received rows, grouped by expert
+#      (`ffn(expert, rows) -> f32 outputs`, the caller's K3/K4 launch);
+#   4. a second all_to_all_single returns the outputs in the received order;
+#   5. the source combines out[t] = h[t] + sum_j w[t, j] * y[t, j] in slot
+#      order j — the single-GPU combine, so the result is bit-identical to one
+#      rank computing every expert (given an ffn whose rows are independent).
+
+def _exchange(send: torch.Tensor, send_counts: list, group) -> tuple:
+    """Variable-split all_to_all_single of the rows of `send` (grouped by
+    destination); returns (received rows, receive counts)."""
+    import torch.distributed as dist
+    G = len(send_counts)
+    dev = send.device
+    cnt = torch.tensor(send_counts, dtype=torch.int64)
+    rcnt = torch.empty(G, dtype=torch.int64)
+    stage = dist.get_backend(group) == "gloo"
+    if stage:
+        dist.all_to_all_single(rcnt, cnt, group=group)
+    else:
+        c_d, r_d = cnt.to(dev), rcnt.to(dev)
+        dist.all_to_all_single(r_d, c_d, group=group)
+        rcnt = r_d.cpu()
+    recv_counts = [int(c) for c in rcnt.tolist()]
+    width = send.shape[1:]
+    src = send.cpu() if (stage and send.is_cuda) else send
+    recv = torch.empty((sum(recv_counts), *width), dtype=send.dtype, device=src.device)
+    dist.all_to_all_single(recv, src.contiguous(), output_split_sizes=recv_counts, input_split_sizes=send_counts,
+                           group=group)
+    return (recv.to(dev) if recv.device != dev else recv), recv_counts
+
+
+def dispatch_combine(a: torch.Tensor, idx: torch.Tensor, w: torch.Tensor, resid: torch.Tensor, cfg: "EPConfig",
+                     ffn, M: int) -> tuple:
+    """One MoE layer with token dispatch: a [T, d] (bf16) normed activations
+    of THIS rank's tokens, idx / w [T, k] their routing, resid [T, d] the
+    residual.  ffn(expert, rows [n, d] bf16) -> [n, d] f32 for an expert this
+    rank owns.  Returns (out [T, d] bf16 = resid + sum_j w_j y_j, stats)."""
+    G, rank = cfg.world, cfg.rank
+    T, k = idx.shape
+    d = a.shape[1]
+    dev = a.device
+    idx_l = idx.to(torch.int64).cpu()
+    flat_e = idx_l.reshape(-1)                                   # row r = (token r // k, slot r % k)
+    dest = flat_e % G
+    # stable order: destination, then expert, then (token, slot)
+    key = (dest * M + flat_e) * (T * k) + torch.arange(T * k)
+    order = torch.argsort(key)
+    send_counts = [int((dest == g).sum()) for g in range(G)]
+    rows = a.reshape(T, 1, d).expand(T, k, d).reshape(T * k, d)[order.to(dev)]
+    ids = flat_e[order].to(torch.int32).reshape(-1, 1)
+    recv_rows, recv_counts = _exchange(rows, send_counts, cfg.group)
+    recv_ids, _ = _exchange(ids.to(dev) if dev.type == "cuda" and not _gloo(cfg) else ids, send_counts, cfg.group)
+    recv_ids = recv_ids.reshape(-1).cpu()
+    y = torch.empty((recv_rows.shape[0], d), dtype=torch.float32, device=dev)
+    experts = sorted(set(recv_ids.tolist()))
+    for e in experts:
+        if owner(e, G) != rank:
+            raise RuntimeError(f"rank {rank} received rows for expert {e} it does not own")
+        sel = torch.nonzero(recv_ids == e).reshape(-1).to(dev)
+        y[sel] = ffn(e, recv_rows[sel])
+    back, _ = _exchange(y, recv_counts, cfg.group)              # outputs return in the sent order
+    y_rows = torch.empty((T * k, d), dtype=torch.float32, device=dev)
+    y_rows[order.to(dev)] = back
+    y_tk = y_rows.view(T, k, d)
+    acc = torch.zeros((T, d), dtype=torch.float32, device=dev)
+    wf = w.to(torch.float32)
+    for j in range(k):
+        acc = acc + wf[:, j:j + 1] * y_tk[:, j]
+    out = (resid.float() + acc).to(torch.bfloat16)
+    return out, {"sent_rows": send_counts, "recv_rows": recv_counts, "experts_run": experts}
+
+
+def _gloo(cfg: "EPConfig") -> bool:
+    import torch.distributed as dist
+    return dist.get_backend(cfg.group) == "gloo"

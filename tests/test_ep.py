@@ -82,3 +82,63 @@ def test_all_reduce_and_all_to_all_combine_bit_identical_world2():
     for p in procs:
         p.join(timeout=60)
     assert all(ok for _, ok in res), res
+
+
+def _dispatch_worker(rank, world, port, q):
+    """Tokens partitioned over the ranks, experts sharded: dispatch rows to the
+    owners over all_to_all, compute there, return and combine — equal to one
+    process computing everything (integer-valued data, so f32 sums are exact
+    and row-independent)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = EP.EPConfig.from_env()
+    g = torch.Generator().manual_seed(0)
+    B_tok, k, M, d = 29, 2, 8, 32
+    a_all = torch.randint(-4, 5, (B_tok * world, d), generator=g).to(torch.bfloat16)
+    idx_all = torch.stack([torch.randperm(M, generator=g)[:k].sort().values for _ in range(B_tok * world)])
+    w_all = torch.randint(1, 4, (B_tok * world, k), generator=g).float() / 4
+    h_all = torch.randint(-8, 9, (B_tok * world, d), generator=g).to(torch.bfloat16)
+    W = torch.randint(-2, 3, (M, d, d), generator=g).float()
+
+    def ffn(e, rows):
+        return rows.float() @ W[e]
+
+    mine = slice(rank * B_tok, (rank + 1) * B_tok)
+    out, st = EP.dispatch_combine(a_all[mine], idx_all[mine].to(torch.int32), w_all[mine], h_all[mine], cfg, ffn, M)
+    ref = torch.zeros((B_tok, d))
+    for j in range(k):
+        for t in range(B_tok):
+            tt = rank * B_tok + t
+            ref[t] += w_all[tt, j] * ffn(int(idx_all[tt, j]), a_all[tt:tt + 1])[0]
+    ref = (h_all[mine].float() + ref).to(torch.bfloat16)
+    ok = bool(torch.equal(out, ref)) and all(EP.owner(e, world) == rank for e in st["experts_run"])
+    ok = ok and sum(st["sent_rows"]) == B_tok * k
+    q.put((rank, ok, st["recv_rows"]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_token_dispatch_all_to_all(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dispatch_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok, _ in res), res
+
+
+def test_all_reduce_and_all_to_all_combine_bit_identical_world4():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 4, port, q)) for r in range(4)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok in res), res
