@@ -256,6 +256,11 @@ int ds_link_trace(ds_link *link, int enable);
 int ds_link_trace_read(ds_link *link, void *ref_event, float *start_ms, float *end_ms, size_t max_spans,
                        size_t *n_out);
 
+/* Diagnostics: per-CTA %globaltimer stamps (ns; [n_ctas][8]: entry, phase A
+ * consumed, grid barrier passed, h staged, exit) of the last fused K4 v6
+ * launch made with DS_K4_V6_TIMELINE=1 in the environment. */
+int ds_debug_k4v6_timeline(unsigned long long *out, int n_ctas);
+
 /* SM-driven host->HBM copy: `ctas` CTAs stream `bytes` from mapped pinned host
  * memory (cudaHostAlloc / cudaHostRegister, UVA) over PCIe with 16-byte loads
  * and streaming stores into `dst` on `stream`.  An alternative to the copy

@@ -44,6 +44,10 @@ int num_sms();
 // the gate (A/B runs).
 unsigned gate_hold(cudaStream_t st);
 void gate_release(unsigned seq);
+// true once a call path `key` has run before: its kernels are then loaded
+// (CUDA lazy loading may synchronise the context on a kernel's first use,
+// which would deadlock against a held stream — the first call is not gated)
+bool gate_warm(uint64_t key);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 

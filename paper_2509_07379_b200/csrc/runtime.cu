@@ -8,6 +8,7 @@
 
 #include <atomic>
 #include <mutex>
+#include <set>
 
 namespace ds {
 
@@ -68,6 +69,16 @@ GateState* gate_state() {
     return &g_gate[dev];
 }
 }  // namespace
+
+bool gate_warm(uint64_t key) {
+    static std::mutex mu;
+    static std::set<uint64_t> seen;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    key = key * 31 + (uint64_t)dev;
+    std::lock_guard<std::mutex> lk(mu);
+    return !seen.insert(key).second;
+}
 
 unsigned gate_hold(cudaStream_t st) {
     GateState* g = gate_state();

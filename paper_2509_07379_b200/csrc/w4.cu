@@ -1207,6 +1207,420 @@ static int staged_mma_launch(const __nv_bfloat16* x, W4Ptr a, W4Ptr b, int N, __
     return DS_OK;
 }
 
+// ------------------------------------------ K4 v6: one persistent launch per expert
+// (R = 1, G = 128).  The SwiGLU GEMV (phase A: 16-row tiles of W1 and W3,
+// the tensor-core consumer of staged_mma_swiglu_kernel) and the down GEMV
+// (phase B: 8-row tiles of W2, 16 consumer warps as 8 rows x 2 K-halves, the
+// FHFMA dot product with h read through L1) run in ONE cooperative launch
+// with a grid barrier between them.  Tickets run over phase-A then phase-B
+// tiles, so each producer streams W2 tiles into its ring as soon as phase A
+// is handed out — the down projection's bytes land while the SwiGLU phase
+// drains, and the second launch's ramp / first-byte latency disappears.
+// The consumers cross the barrier (all h written) on their first phase-B
+// stage, compute the per-32 sums of h once, and consume the staged W2 tiles.
+namespace k4f {
+constexpr int kConsumers = 16;
+constexpr int kThreads = 32 * (kConsumers + 1);
+constexpr int RBA = 16, RBB = 8;
+constexpr int kSmemCap = 227 * 1024;
+
+template <int KA, int KB>
+struct Geo {
+    static constexpr int GPRA = KA / 128, CODEA = KA / 2, SCA = GPRA * 2;
+    static constexpr int ZA = (RBA * GPRA / 2 + 32 + 15) & ~15;
+    static constexpr int MATA = RBA * CODEA + RBA * SCA + ZA;
+    static constexpr int STAGEA = 2 * MATA;
+    static constexpr int GPRB = KB / 128, CODEB = KB / 2, SCB = GPRB * 2;
+    static constexpr int ZB = (RBB * GPRB / 2 + 32 + 15) & ~15;
+    static constexpr int STAGEB = RBB * CODEB + RBB * SCB + ZB;
+    static constexpr int SLOT = ((STAGEA > STAGEB ? STAGEA : STAGEB) + 127) & ~127;
+    static constexpr int NCHB = KB / 32;                       // 32-code chunks of a W2 row
+    static constexpr int CPLB = NCHB / 2 / 32;                 // chunks per lane per K-half
+    static constexpr int XA = KA * 2 + GPRA * 4;               // phase A: x + per-group sums
+    static constexpr int XREG = ((XA > NCHB * 4 ? XA : NCHB * 4) + 127) & ~127;   // phase B: per-32 sums of h
+    // phase B keeps h (KB bf16 = 64 B per 32-chunk) in shared memory: the x
+    // region after the per-chunk sums, then the tail of every ring slot (a
+    // phase-B stage is smaller than a phase-A stage)
+    static constexpr int HX_OFF = (NCHB * 4 + 127) & ~127;
+    static constexpr int HX_CH = (XREG - HX_OFF) / 64;                  // chunks in the x region
+    static constexpr int HT_OFF = (STAGEB + 127) & ~127;
+    static constexpr int HT_CH = (SLOT - HT_OFF) / 64;                  // chunks per slot tail
+    static constexpr int RED = 2 * kConsumers * 2 * 16 * 4 + 2 * RBB * 2 * 4;
+    static constexpr int FIXED = XREG + RED + 64;
+    static constexpr int stages() {
+        int n = (kSmemCap - FIXED) / (SLOT + 24);
+        return n > 6 ? 6 : n;
+    }
+    static constexpr size_t smem(int S) { return (size_t)FIXED + (size_t)S * (SLOT + 24); }
+    static constexpr bool h_fits(int S) { return HX_CH + S * HT_CH >= NCHB; }
+};
+}  // namespace k4f
+
+__device__ unsigned g_k4f_bar[k4s::kTicketSlots];
+// diagnostics (DS_K4_V6_TIMELINE=1): per-CTA %globaltimer stamps of the last
+// launch — entry, phase A consumed, grid barrier passed, h staged, exit
+__device__ unsigned long long g_k4f_dbg[1024 * 8];
+__device__ unsigned g_k4f_exit[k4s::kTicketSlots];
+
+template <int KA, int KB>
+__global__ void __launch_bounds__(k4f::kThreads, 1) expert_fused_v6_kernel(
+    const __nv_bfloat16* __restrict__ x, W4Ptr w1, W4Ptr w3, W4Ptr w2, int S, __nv_bfloat16* __restrict__ hout,
+    const float* __restrict__ route_w, float* __restrict__ out, unsigned slot_id, int dbg) {
+    using namespace ds::sm100;
+    using Gm = k4f::Geo<KA, KB>;
+    auto stamp = [&](int i) {
+        if (dbg && threadIdx.x == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            g_k4f_dbg[blockIdx.x * 8 + i] = t;
+        }
+    };
+    stamp(0);
+    constexpr int GPRA = Gm::GPRA, GPRB = Gm::GPRB;
+    constexpr int TA = KB / k4f::RBA;                 // phase-A tiles: rows of W1 / W3 (N = ff = KB)
+    constexpr int TB = KA / k4f::RBB;                 // phase-B tiles: rows of W2 (N = d = KA)
+    constexpr int T = TA + TB;
+    constexpr int GPW = GPRA / k4f::kConsumers;       // phase A: quantisation groups per warp
+    static_assert(GPRA % k4f::kConsumers == 0, "phase A K split must be whole groups");
+    static_assert((Gm::NCHB / 2) % 32 == 0, "phase B K halves must be whole lane chunks");
+    extern __shared__ __align__(128) uint8_t smem[];
+    const __nv_bfloat16* xs = reinterpret_cast<const __nv_bfloat16*>(smem);
+    float* xgs = reinterpret_cast<float*>(smem + KA * 2);          // phase A: sum of x per group
+    float* hsum = reinterpret_cast<float*>(smem);                  // phase B: sum of h per 32-chunk (aliases x)
+    float* red = reinterpret_cast<float*>(smem + Gm::XREG);        // [2][16 warps][2 mats][16 rows]
+    float* redb = red + 2 * k4f::kConsumers * 2 * 16;              // [2][8 rows][2 halves]
+    uint8_t* stages = smem + Gm::FIXED;
+    uint64_t* full = reinterpret_cast<uint64_t*>(stages + (size_t)S * Gm::SLOT);
+    uint64_t* empty = full + S;
+    int* hdr = reinterpret_cast<int*>(empty + S);
+    auto h_chunk = [&](int c) -> uint4* {       // 64-byte chunk c of h in shared memory (phase B)
+        if (c < Gm::HX_CH) return reinterpret_cast<uint4*>(smem + Gm::HX_OFF + 64 * c);
+        c -= Gm::HX_CH;
+        const int sl = c / Gm::HT_CH;
+        return reinterpret_cast<uint4*>(stages + (size_t)sl * Gm::SLOT + Gm::HT_OFF + 64 * (c - sl * Gm::HT_CH));
+    };
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], k4f::kConsumers);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == k4f::kConsumers) {                                 // producer
+        if (lane != 0) return;
+        unsigned* tk = g_k4s_ticket + slot_id;
+        const uint64_t pol = l2_evict_first_policy();
+        const int first = (int)atomicAdd(tk, (unsigned)S);
+        int pending = -1;
+        for (int s = 0;; ++s) {
+            const int slot = s % S;
+            if (s >= S) mbar_wait(&empty[slot], ((s / S) - 1) & 1);
+            int t = s < S ? first + s : pending;
+            if (s >= S - 1 && t < T) {
+                pending = (int)atomicAdd(tk, 1u);
+                if (pending >= TA && pending < T) {
+                    // the next W2 tile is ours: pull it into L2 now, so its bulk copy (issued once a
+                    // slot frees, typically after the phase barrier) hits L2
+                    const int rp = (pending - TA) * k4f::RBB;
+                    bulk_prefetch_l2(reinterpret_cast<const uint8_t*>(w2.codes) + (size_t)rp * Gm::CODEB,
+                                     k4f::RBB * Gm::CODEB);
+                    bulk_prefetch_l2(reinterpret_cast<const uint8_t*>(w2.scales) + (size_t)rp * Gm::SCB,
+                                     k4f::RBB * Gm::SCB);
+                }
+            }
+            if (t >= T || t < 0) {
+                hdr[slot] = -1;
+                mbar_arrive(&full[slot]);
+                break;
+            }
+            hdr[slot] = t;
+            uint8_t* dst = stages + (size_t)slot * Gm::SLOT;
+            if (t < TA) {
+                const int r0 = t * k4f::RBA;
+                const uint32_t zb0 = ((uint32_t)(r0 * GPRA) >> 1) & ~15u;
+                const uint32_t zb1 = (((uint32_t)((r0 + k4f::RBA) * GPRA) >> 1) + 15u) & ~15u;
+                const uint32_t cb = k4f::RBA * Gm::CODEA, sb = k4f::RBA * Gm::SCA, zb = zb1 - zb0;
+                mbar_expect_tx(&full[slot], 2 * (cb + sb + zb));
+                const W4Ptr W[2] = {w1, w3};
+#pragma unroll
+                for (int m = 0; m < 2; ++m) {
+                    uint8_t* md = dst + m * Gm::MATA;
+                    bulk_load(md, reinterpret_cast<const uint8_t*>(W[m].codes) + (size_t)r0 * Gm::CODEA, cb,
+                              &full[slot], pol);
+                    bulk_load(md + cb, reinterpret_cast<const uint8_t*>(W[m].scales) + (size_t)r0 * Gm::SCA, sb,
+                              &full[slot], pol);
+                    bulk_load(md + cb + sb, W[m].zeros + zb0, zb, &full[slot], pol);
+                }
+            } else {
+                const int r0 = (t - TA) * k4f::RBB;
+                const uint32_t zb0 = ((uint32_t)(r0 * GPRB) >> 1) & ~15u;
+                const uint32_t zb1 = (((uint32_t)((r0 + k4f::RBB) * GPRB) >> 1) + 15u) & ~15u;
+                const uint32_t cb = k4f::RBB * Gm::CODEB, sb = k4f::RBB * Gm::SCB, zb = zb1 - zb0;
+                mbar_expect_tx(&full[slot], cb + sb + zb);
+                bulk_load(dst, reinterpret_cast<const uint8_t*>(w2.codes) + (size_t)r0 * Gm::CODEB, cb, &full[slot],
+                          pol);
+                bulk_load(dst + cb, reinterpret_cast<const uint8_t*>(w2.scales) + (size_t)r0 * Gm::SCB, sb,
+                          &full[slot], pol);
+                bulk_load(dst + cb + sb, w2.zeros + zb0, zb, &full[slot], pol);
+            }
+        }
+        __threadfence();
+        if (atomicAdd(g_k4s_done + slot_id, 1u) == gridDim.x - 1) {   // every ticket of the launch is taken
+            atomicExch(tk, 0u);
+            atomicExch(g_k4s_done + slot_id, 0u);
+        }
+        return;
+    }
+
+    {   // phase A input: x -> shared memory (plain layout) and per-group sums
+        constexpr int NT = 32 * k4f::kConsumers;
+        constexpr int UNITS = KA / 8;
+        constexpr int PER = (UNITS + NT - 1) / NT;
+        const uint4* xu = reinterpret_cast<const uint4*>(x);
+        uint4 v[PER];
+#pragma unroll
+        for (int j = 0; j < PER; ++j)
+            if (threadIdx.x + j * NT < UNITS) v[j] = __ldg(xu + threadIdx.x + j * NT);
+#pragma unroll
+        for (int j = 0; j < PER; ++j)
+            if (threadIdx.x + j * NT < UNITS) reinterpret_cast<uint4*>(smem)[threadIdx.x + j * NT] = v[j];
+        asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+        for (int j = warp; j < GPRA; j += k4f::kConsumers) {
+            const uint32_t* p = reinterpret_cast<const uint32_t*>(xs + 128 * j) + 2 * lane;
+            float s_ = (bf16_lo(p[0]) + bf16_hi(p[0])) + (bf16_lo(p[1]) + bf16_hi(p[1]));
+            s_ = warp_sum(s_);
+            if (lane == 0) xgs[j] = s_;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+    }
+    const int g = lane >> 2, tq = lane & 3;
+    bool crossed = false;
+    int ita = 0, itb = 0;
+    for (int s = 0;; ++s) {
+        const int slot = s % S;
+        mbar_wait(&full[slot], (s / S) & 1);
+        const int t = hdr[slot];
+        const uint8_t* base = stages + (size_t)slot * Gm::SLOT;
+        if (t >= 0 && t < TA) {                                    // ---- phase A: SwiGLU tile
+            const int r0 = t * k4f::RBA;
+            const uint32_t zb0 = ((uint32_t)(r0 * GPRA) >> 1) & ~15u;
+            float acc[2][2] = {};
+#pragma unroll
+            for (int jj = 0; jj < GPW; ++jj) {
+                const int j = warp * GPW + jj;
+                uint4 xv[4];
+                const uint4* xp = reinterpret_cast<const uint4*>(xs + 128 * j + 32 * tq);
+#pragma unroll
+                for (int w = 0; w < 4; ++w) xv[w] = xp[w];
+                uint4 c[2][2];
+#pragma unroll
+                for (int m = 0; m < 2; ++m)
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh)
+                        c[m][hh] = *reinterpret_cast<const uint4*>(base + m * Gm::MATA + (g + 8 * hh) * Gm::CODEA +
+                                                                   (4 * j + tq) * 16);
+                float dd[2][4] = {};
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                    const uint32_t xw[4] = {xv[w].x, xv[w].y, xv[w].z, xv[w].w};
+#pragma unroll
+                    for (int s2 = 0; s2 < 2; ++s2) {
+#pragma unroll
+                        for (int m = 0; m < 2; ++m) {
+                            const uint32_t* cg = reinterpret_cast<const uint32_t*>(&c[m][0]);
+                            const uint32_t* cg8 = reinterpret_cast<const uint32_t*>(&c[m][1]);
+                            mma16816(dd[m], nib_pair_magic(cg[w] >> (8 * s2)), nib_pair_magic(cg8[w] >> (8 * s2)),
+                                     nib_pair_magic(cg[w] >> (8 * s2 + 4)), nib_pair_magic(cg8[w] >> (8 * s2 + 4)),
+                                     xw[2 * s2], xw[2 * s2 + 1]);
+                        }
+                    }
+                }
+                const float xg = xgs[j];
+#pragma unroll
+                for (int m = 0; m < 2; ++m) {
+                    const uint8_t* mb = base + m * Gm::MATA;
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh) {
+                        const int row = g + 8 * hh;
+                        const uint16_t sv = reinterpret_cast<const uint16_t*>(mb + k4f::RBA * Gm::CODEA +
+                                                                              row * Gm::SCA)[j];
+                        const uint32_t zn = (uint32_t)((r0 + row) * GPRA + j);
+                        const uint32_t zq = ((uint32_t)mb[k4f::RBA * (Gm::CODEA + Gm::SCA) + (zn >> 1) - zb0] >>
+                                             ((zn & 1) << 2)) & 15u;
+                        const float z128 = __uint_as_float(0x43000000u | (zq << 16));
+                        const float sc = __uint_as_float((uint32_t)sv << 16);
+                        acc[m][hh] = fmaf(sc, fmaf(-z128, xg, dd[m][2 * hh]), acc[m][hh]);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[slot]);
+            float* rd = red + (size_t)(ita & 1) * k4f::kConsumers * 2 * 16;
+            if (tq == 0) {
+#pragma unroll
+                for (int m = 0; m < 2; ++m) {
+                    rd[(warp * 2 + m) * 16 + g] = acc[m][0];
+                    rd[(warp * 2 + m) * 16 + g + 8] = acc[m][1];
+                }
+            }
+            asm volatile("bar.sync 2, %0;" ::"n"(32 * k4f::kConsumers) : "memory");
+            if (warp == 0 && lane < 16) {
+                float av = 0.f, bv = 0.f;
+#pragma unroll
+                for (int w = 0; w < k4f::kConsumers; ++w) {
+                    av += rd[(w * 2 + 0) * 16 + lane];
+                    bv += rd[(w * 2 + 1) * 16 + lane];
+                }
+                hout[r0 + lane] = __float2bfloat16_rn(av / (1.0f + expf(-av)) * bv);
+            }
+            ++ita;
+            continue;
+        }
+        if (!crossed) {                                            // ---- phase boundary (grid barrier)
+            asm volatile("bar.sync 3, %0;" ::"n"(32 * k4f::kConsumers) : "memory");   // this CTA's h is written
+            stamp(1);
+            if (threadIdx.x == 0) {
+                __threadfence();
+                atomicAdd(g_k4f_bar + slot_id, 1u);
+            }
+            crossed = true;
+            if (t < 0) break;
+            if (threadIdx.x == 0) {
+                unsigned v;
+                do {
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(g_k4f_bar + slot_id));
+                } while (v < gridDim.x);
+            }
+            stamp(2);
+            asm volatile("bar.sync 3, %0;" ::"n"(32 * k4f::kConsumers) : "memory");
+            for (int i = threadIdx.x; i < Gm::NCHB; i += 32 * k4f::kConsumers) {   // h -> smem, per-32 sums
+                const uint4* hp = reinterpret_cast<const uint4*>(hout) + 4 * i;
+                uint4 v[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) v[q] = __ldcg(hp + q);
+                uint4* dst = h_chunk(i);
+                float s_ = 0.f;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    dst[q ^ ((i >> 1) & 3)] = v[q];     // 8 consecutive chunks hit 8 distinct 16-B bank groups
+                    const uint32_t vv[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) s_ += bf16_lo(vv[u]) + bf16_hi(vv[u]);
+                }
+                hsum[i] = s_;
+            }
+            asm volatile("bar.sync 3, %0;" ::"n"(32 * k4f::kConsumers) : "memory");
+            stamp(3);
+        }
+        if (t < 0) break;
+        {                                                          // ---- phase B: down tile
+            const int r0 = (t - TA) * k4f::RBB;
+            const int r = warp & (k4f::RBB - 1), hf = warp / k4f::RBB;
+            const int n = r0 + r;
+            const uint32_t zb0 = ((uint32_t)(r0 * GPRB) >> 1) & ~15u;
+            const float o_prev = (hf == 0 && lane == 0) ? out[n] : 0.f;   // in flight during the dot product
+            float acc = 0.f;
+#pragma unroll
+            for (int i = 0; i < Gm::CPLB; ++i) {
+                const int c = hf * (Gm::NCHB / 2) + lane + 32 * i;
+                const int gq = c >> 2;
+                const uint4* hp = h_chunk(c);
+                uint4 xv[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) xv[q] = hp[q ^ ((c >> 1) & 3)];
+                const float xsm = hsum[c];
+                const uint4 c4 = *reinterpret_cast<const uint4*>(base + r * Gm::CODEB + c * 16);
+                const uint16_t sv = reinterpret_cast<const uint16_t*>(base + k4f::RBB * Gm::CODEB + r * Gm::SCB)[gq];
+                const uint32_t zn = (uint32_t)(n * GPRB + gq);
+                const uint8_t zv = base[k4f::RBB * (Gm::CODEB + Gm::SCB) + (zn >> 1) - zb0];
+                const uint32_t cw[4] = {c4.x, c4.y, c4.z, c4.w};
+                float pp[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int ii = 0; ii < 4; ++ii) {
+                    const uint32_t xx[4] = {xv[ii].x, xv[ii].y, xv[ii].z, xv[ii].w};
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint32_t pr = nib_pair_magic(cw[ii] >> (4 * q));
+                        fma_bf16_lo(pp[(q & 1) * 2], pr, xx[q]);
+                        fma_bf16_hi(pp[(q & 1) * 2 + 1], pr, xx[q]);
+                    }
+                }
+                const float z128 = __uint_as_float(0x43000000u | ((((uint32_t)zv >> ((zn & 1) << 2)) & 15u) << 16));
+                const float sc = __uint_as_float((uint32_t)sv << 16);
+                acc = fmaf(sc, ((pp[0] + pp[1]) + (pp[2] + pp[3])) - z128 * xsm, acc);
+            }
+            acc = warp_sum(acc);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[slot]);
+            float* rb = redb + (itb & 1) * k4f::RBB * 2;
+            if (lane == 0) rb[r * 2 + hf] = acc;
+            asm volatile("bar.sync 4, %0;" ::"n"(32 * k4f::kConsumers) : "memory");
+            if (hf == 0 && lane == 0)
+                out[n] = __fadd_rn(o_prev, __fmul_rn(route_w[0], rb[r * 2 + 0] + rb[r * 2 + 1]));
+            ++itb;
+        }
+    }
+    // last CTA out resets the grid-barrier counter of this ticket slot
+    asm volatile("bar.sync 3, %0;" ::"n"(32 * k4f::kConsumers) : "memory");
+    stamp(4);
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(g_k4f_exit + slot_id, 1u) == gridDim.x - 1) {
+            atomicExch(g_k4f_bar + slot_id, 0u);
+            atomicExch(g_k4f_exit + slot_id, 0u);
+        }
+    }
+}
+
+template <int KA, int KB>
+static int expert_v6_launch(const __nv_bfloat16* x, const ds_w4_expert* e, __nv_bfloat16* h, const float* rw,
+                            float* acc, cudaStream_t st) {
+    using Gm = k4f::Geo<KA, KB>;
+    constexpr int S = Gm::stages();
+    if constexpr (S < 3 || !Gm::h_fits(S)) {
+        return 1;
+    } else {
+        static bool init = false;
+        const size_t smem = Gm::smem(S);
+        if (!init) {
+            cudaFuncSetAttribute(expert_fused_v6_kernel<KA, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+            init = true;
+        }
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(num_sms());
+        cfg.blockDim = dim3(k4f::kThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeCooperative;     // the grid barrier needs every CTA resident
+        at[0].val.cooperative = 1;
+        cfg.attrs = at;
+        static const bool coop = !(getenv("DS_K4_V6_COOP") && getenv("DS_K4_V6_COOP")[0] == '0');   // A/B runs
+        cfg.numAttrs = coop ? 1 : 0;
+        const unsigned slot_id = k4s_next_slot();
+        static const int dbg = getenv("DS_K4_V6_TIMELINE") ? 1 : 0;
+        cudaError_t er = cudaLaunchKernelEx(&cfg, expert_fused_v6_kernel<KA, KB>, x, to_ptr(e->w1), to_ptr(e->w3),
+                                            to_ptr(e->w2), S, h, rw, acc, slot_id, dbg);
+        return er == cudaSuccess ? DS_OK : cuda_status(er, "ds_w4_expert_gemv (v6 fused)");
+    }
+}
+
+// v6 for the shapes it is instantiated for; 1 = not applicable (caller uses v5)
+static int expert_v6(const void* x, int R, const ds_w4_expert* e, int d, int ff, int G, void* h, const float* rw,
+                     float* acc, cudaStream_t st) {
+    static const bool on = !(getenv("DS_K4_V6") && getenv("DS_K4_V6")[0] == '0');
+    if (!on || R != 1 || G != 128 || !e || !x || !h || !rw || !acc) return 1;
+    if (!check_linear(e->w1) || !check_linear(e->w3) || !check_linear(e->w2)) return 1;
+    const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x);
+    __nv_bfloat16* hb = static_cast<__nv_bfloat16*>(h);
+    if (d == 4096 && ff == 14336) return expert_v6_launch<4096, 14336>(xb, e, hb, rw, acc, st);
+    return 1;
+}
+
 inline bool k4_staged_enabled() {
     static const char* v = getenv("DS_K4_VARIANT");
     return !(v && (v[0] == 'v' || v[0] == 'm'));
@@ -1515,14 +1929,16 @@ extern "C" int ds_w4_expert_gemv(const void* x, int R, const ds_w4_expert* e, in
     cudaStream_t st = as_stream(stream);
     // with a span requested, hold the stream until both launches are queued
     // (the span then excludes host submission latency; see gate_hold)
-    const unsigned gate = ev_start ? gate_hold(st) : 0;
+    const uint64_t key = (((1ull * 64 + (uint64_t)R) * 65536 + (uint64_t)d) * 65536 + (uint64_t)ff) * 256 + (uint64_t)G;
+    const unsigned gate = (ev_start && gate_warm(key)) ? gate_hold(st) : 0;
     int rc = DS_OK;
     if (ev_start) {
         cudaError_t er = cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_start), st);
         if (er != cudaSuccess) rc = cuda_status(er, "ds_w4_expert_gemv: event");
     }
-    if (!rc) rc = expert_gemv_fused(x, R, e, d, ff, G, h, route_w, acc, st);
-    if (rc > 0 && rc == 1) {        // no fused variant for this shape: the two-kernel path
+    if (!rc) rc = expert_v6(x, R, e, d, ff, G, h, route_w, acc, st);
+    if (rc == 1) rc = expert_gemv_fused(x, R, e, d, ff, G, h, route_w, acc, st);
+    if (rc == 1) {        // no fused variant for this shape: the two-kernel path
         rc = ds_w4_swiglu_gemv(x, R, e, d, ff, G, h, stream);
         if (!rc) rc = ds_w4_down_gemv(h, R, e, d, ff, G, route_w, route_stride, acc, stream);
     }
@@ -1546,4 +1962,12 @@ extern "C" int ds_combine_finalize(float* acc, const void* resid, int R, int d, 
                                                          (__nv_bfloat16*)out);
     DS_LAUNCH_CHECK("ds_combine_finalize");
     return DS_OK;
+}
+
+// Diagnostics: the per-CTA stamps of the last v6 launch run with DS_K4_V6_TIMELINE=1
+// ([n_ctas][8] u64 globaltimer ns; see expert_fused_v6_kernel).
+extern "C" int ds_debug_k4v6_timeline(unsigned long long* out, int n_ctas) {
+    DS_CHECK_ARG(out && n_ctas > 0 && n_ctas <= 1024, "ds_debug_k4v6_timeline: bad arguments");
+    cudaError_t e = cudaMemcpyFromSymbol(out, g_k4f_dbg, (size_t)n_ctas * 8 * sizeof(unsigned long long));
+    return cuda_status(e, "ds_debug_k4v6_timeline");
 }

@@ -570,7 +570,9 @@ static int grouped_ffn_impl(const void* xperm, const int32_t* offsets, int E, co
     // host-side preparation (tensor maps, argument blocks) stays outside the
     // timed span, and the stream is held until every launch is queued (the
     // span covers device execution only; see gate_hold)
-    const unsigned gate = ev_start ? gate_hold(st) : 0;
+    const uint64_t key = ((((2ull * 512 + (uint64_t)TN) * 65536 + (uint64_t)d) * 65536 + (uint64_t)ff) * 256 +
+                          (uint64_t)G) * 2 + (splits > 1);
+    const unsigned gate = (ev_start && gate_warm(key)) ? gate_hold(st) : 0;
     if (ev_start) {
         cudaError_t er = cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_start), st);
         if (er != cudaSuccess) rc = cuda_status(er, "ds_w4_grouped_ffn: event");

@@ -203,9 +203,11 @@ def test_w4_grouped_ffn_tcgen05(d, ff, rows, cuda):
 
 
 def test_expert_gemv_and_timed_grouped_ffn_match_split_calls(cuda):
-    """ds_w4_expert_gemv (SwiGLU + PDL down in one call, native timing events)
-    equals the two separate calls bit for bit; ds_w4_grouped_ffn_ev equals
-    ds_w4_grouped_ffn and records a positive span."""
+    """ds_w4_expert_gemv (one call: the fused v6 launch at 8x7B shapes, else
+    SwiGLU + PDL down; native timing events) gives the separate calls' h bit
+    for bit and their output to f32 summation order (v6 splits the down
+    projection's K in halves); ds_w4_grouped_ffn_ev equals ds_w4_grouped_ffn
+    and records a positive span."""
     import torch
     from paper_2509_07379_b200 import ops
     d, ff, G = 4096, 14336, 128
@@ -224,7 +226,8 @@ def test_expert_gemv_and_timed_grouped_ffn_match_split_calls(cuda):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ops.expert_gemv(x, e, d, ff, G, h2, rw, 1, a2, ev0, ev1)
     torch.cuda.synchronize()
-    assert torch.equal(h1, h2) and torch.equal(a1, a2)
+    assert torch.equal(h1, h2)
+    assert ((a1 - a2).norm() / a1.norm()).item() < 1e-6
     assert ev0.elapsed_time(ev1) > 0
     R = 128
     xp = _rand_bf16((R, d), 1.0, torch.Generator().manual_seed(4)).to(cuda)
