@@ -290,12 +290,35 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
         uint16_t* sc_s = reinterpret_cast<uint16_t*>(smem + args.sc_off);
         uint8_t* z_s = smem + args.z_off;
         const int ngs = args.ng_stride;
-        // stage the n-block's scales and zeros for the whole k-range once
-        for (int i = td; i < NMAT * BM * ng; i += kDequantThreads) {
-            const int j = i / (BM * ng), rem = i - j * BM * ng, r = rem / ng, g = rem - r * ng;
-            const size_t gi = (size_t)(n0 + r) * gpr + g0 + g;
-            sc_s[(j * BM + r) * ngs + g] = __ldg(W[j].scales + gi);
-            z_s[(j * BM + r) * ngs + g] = (__ldg(W[j].zeros + (gi >> 1)) >> ((gi & 1) * 4)) & 15;
+        // stage the n-block's scales and zeros for the whole k-range once;
+        // batches of 8 independent loads per thread are issued before any
+        // store, so the prologue costs a few memory latencies, not one per element
+        {
+            const int total = NMAT * BM * ng;
+            constexpr int B8 = 8;
+            for (int base = td; base < total; base += B8 * kDequantThreads) {
+                uint16_t sv[B8];
+                uint8_t zv[B8];
+                int dst[B8];
+#pragma unroll
+                for (int u = 0; u < B8; ++u) {
+                    const int i = base + u * kDequantThreads;
+                    dst[u] = -1;
+                    if (i < total) {
+                        const int j = i / (BM * ng), rem = i - j * BM * ng, r = rem / ng, g = rem - r * ng;
+                        const size_t gi = (size_t)(n0 + r) * gpr + g0 + g;
+                        sv[u] = __ldg(W[j].scales + gi);
+                        zv[u] = (__ldg(W[j].zeros + (gi >> 1)) >> ((gi & 1) * 4)) & 15;
+                        dst[u] = (j * BM + r) * ngs + g;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < B8; ++u)
+                    if (dst[u] >= 0) {
+                        sc_s[dst[u]] = sv[u];
+                        z_s[dst[u]] = zv[u];
+                    }
+            }
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kDequantThreads));
         const int swz = nl & 7;
