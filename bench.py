@@ -76,6 +76,9 @@ def parse():
                          "shard + cache, NCCL all-reduce combine) on ONE request instead of N replicas")
     ap.add_argument("--ep-combine", default="allreduce", choices=["allreduce", "alltoall"],
                     help="--ep combine collective: one all-reduce, or all_to_all_single + all-gather")
+    ap.add_argument("--also-22b", type=int, default=1,
+                    help="default 8x7B run on one GPU: also serve one Mixtral-8x22B request (BASELINE configs[2]) "
+                         "in a subprocess after the timed region and attach its line as 'config_8x22b'")
     ap.add_argument("--sweep", action="store_true",
                     help="BASELINE config 4: batch x prompt grid through BatchEngine (one JSON document)")
     ap.add_argument("--sweep-batches", default="1,2,4,8,16,32")
@@ -620,10 +623,50 @@ def run_ours(args):
         line["parity"] = parity_leg(eng, args, shape, net, pop, aff, r0, one_step)
     if not args.no_cpu_baseline and ws == 1:
         line["cpu_baseline"] = cpu_baseline_entry(shape, args.prefill, args.decode)
+    if args.also_22b and ws == 1 and shape.name == "mixtral-8x7b" and args.policy == "duoserve":
+        # free this engine's device and pinned host memory, then BASELINE configs[2] in its own process
+        st_ = eng.store
+        eng.close()
+        del eng, prof, tl, one_step, dense, res, r0
+        st_.close()
+        del st_
+        store = None
+        import gc
+        gc.collect()
+        torch.cuda.empty_cache()
+        if hasattr(torch._C, "_host_emptyCache"):
+            torch._C._host_emptyCache()              # return the cached pinned store to the OS
+        line["config_8x22b"] = run_22b_subprocess(args)
     out = json.dumps(line)
     print(out)
     if args.out:
         Path(args.out).write_text(out + "\n")
+
+
+def run_22b_subprocess(args, timeout_s: int = 900) -> dict:
+    """BASELINE configs[2] (Mixtral-8x22B-shaped W4, batch 1, prefill 512) on
+    this GPU through the same public API, in a child process (its 70 GB
+    pinned expert store and any failure stay out of the headline run): one
+    warm-up and one timed request, decode 32 tokens, auto pinning under the
+    15 % cap, ExpertMLP(seed=0) predictor (no calibration pass)."""
+    cmd = [sys.executable, str(ROOT / "bench.py"), "--config", "mixtral-8x22b", "--steps", "1", "--warmup", "1",
+           "--decode", "32", "--predictor", "random", "--no-cpu-baseline", "--also-22b", "0",
+           "--prefill", str(args.prefill)]
+    t0 = time.time()
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout_s)
+    except subprocess.TimeoutExpired:
+        return {"error": f"timed out after {timeout_s} s"}
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    if r.returncode != 0 or not lines:
+        return {"error": f"rc={r.returncode}", "stderr_tail": r.stderr[-600:]}
+    d = json.loads(lines[-1])
+    keep = ("value", "unit", "ttft_ms", "decode_tok_s", "decode_ms_per_token", "residency", "link", "roofline",
+            "predictor", "pinning", "parity", "clocks", "config", "e2e")
+    out = {k: d[k] for k in keep if k in d}
+    out["command"] = " ".join(cmd[1:])
+    out["wall_s"] = round(time.time() - t0, 1)
+    return out
 
 
 def run_sweep(args):

@@ -283,3 +283,27 @@ def test_staged_gemv_concurrent_streams_and_repeat(cuda):
         if r % 10 == 9 or r == 69:
             torch.cuda.synchronize()
             assert torch.equal(h, ref_h[r % E]) and torch.equal(a, ref_a[r % E]), r
+
+
+def test_cache_check_matches_sim_ref_refetch_rule(cuda):
+    """K7 ds_cache_check (sync point 1 on the device: bit j of miss[t] set when
+    the gate's j-th expert is not in the resident prediction) gives exactly
+    sim_ref's refetch sets for random gate / prediction pairs."""
+    import numpy as np
+    import torch
+    from oracle import sim_ref
+    rng = np.random.default_rng(5)
+    T, k, M, L = 257, 2, 8, 2
+    idx = np.stack([np.sort(rng.choice(M, k, replace=False)) for _ in range(T)]).astype(np.int32)
+    pred = np.stack([np.sort(rng.choice(M, k, replace=False)) for _ in range(T)]).astype(np.int32)
+    di, dp = torch.from_numpy(idx).to(cuda), torch.from_numpy(pred).to(cuda)
+    miss = torch.empty(T, dtype=torch.int32, device=cuda)
+    _lib.call("ds_cache_check", _lib.ptr(di), _lib.ptr(dp), T, k, _lib.ptr(miss), _lib.stream_ptr())
+    torch.cuda.synchronize()
+    got = miss.cpu().numpy()
+    paths = [((0, 1), tuple(int(e) for e in idx[t])) for t in range(T)]
+    preds = [[None, tuple(int(e) for e in pred[t])] for t in range(T)]
+    log, _ = sim_ref.cache_log_decode(paths, preds, L)
+    for t in range(T):
+        ref = log[2 * t + 1]["refetch"]
+        assert [int(idx[t, j]) for j in range(k) if got[t] >> j & 1] == ref, t
