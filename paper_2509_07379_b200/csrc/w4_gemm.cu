@@ -57,6 +57,8 @@ struct GemmArgs {
     CUtensorMap codes_map[kMaxExperts][2];   // [N, K/2] u8 tiles {CK * 32 B, 128 rows}
     int K, N, G;
     int kt_per_split;   // k-tiles (of BK) per split
+    int n_eff;          // UMMA N actually issued (multiple of 16, <= TN): the token rows of a single
+                        // m-block rounded up to 16, so a 151-row expert costs N = 160, not 256
     int splits;
     int total_rows;
     int row_start[kMaxExperts];
@@ -86,8 +88,10 @@ struct Smem {
     // kind::f16 MMA reading both operands from shared memory needs all of its
     // 128 B/clk, leaving nothing for the dequant).  TN = 256 needs every TMEM
     // column for the accumulators, so A stays in shared memory there.
-    static constexpr bool A_TMEM = TN == 128;
-    static constexpr int AS = (NMAT == 2 && TN == 256) ? 2 : 4;
+    // TN = 160 (129..160 token rows, the typical prefill expert at T = 512):
+    // accumulators 2 x 160 columns + 3 A stages x 64 columns = all 512
+    static constexpr bool A_TMEM = TN <= 160;
+    static constexpr int AS = (NMAT == 2 && TN == 256) ? 2 : (TN == 160 ? 3 : 4);
     static constexpr int BS = TN == 256 ? (NMAT == 2 ? 2 : 3) : 4;   // activation stages
     static constexpr int A_STAGE = NMAT * kTileBytes;
     static constexpr int B_STAGE = TN * 128;
@@ -234,14 +238,14 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
             for (int kt = 0; kt < KT; ++kt) {
                 const int s = kt % BS;
                 if (kt >= BS) mbar_wait(&b_empty[s], ((kt / BS) - 1) & 1);
-                mbar_expect_tx(&b_full[s], S::B_STAGE);
+                mbar_expect_tx(&b_full[s], (uint32_t)args.n_eff * 128u);
                 tma_load_2d(smem + S::B_OFF + s * S::B_STAGE, &act_map, &b_full[s], (kt0 + kt) * BK, row_coord);
             }
         }
     } else if (warp == 2) {
         // -------------------------------------------------------- MMA issuer
         if (lane == 0) {
-            const uint32_t idesc = idesc_bf16_f32(BM, TN);
+            const uint32_t idesc = idesc_bf16_f32(BM, args.n_eff);
             for (int kt = 0; kt < KT; ++kt) {
                 const int sa = kt % AS, sb = kt % BS;
                 mbar_wait(&b_full[sb], (kt / BS) & 1);
@@ -371,8 +375,8 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
             tc_fence_after();
             const uint32_t lane_addr = tmem_base + ((uint32_t)(32 * q) << 16);
             const int row0 = args.row_start[e] + m0;
-            const int valid = min(TN, rows - m0);
-            for (int c0 = 0; c0 < TN; c0 += 16) {
+            const int valid = min(args.n_eff, rows - m0);
+            for (int c0 = 0; c0 < args.n_eff; c0 += 16) {
                 uint32_t d1[16];
                 tmem_ld16(lane_addr + c0, d1);
                 if constexpr (NMAT == 2) {
@@ -501,7 +505,7 @@ using namespace ds;
 extern "C" size_t ds_w4_grouped_ffn_workspace(int total_rows, int d, int ff) {
     // worst case over the token tile (128 or 256 rows) and G: fewer m-blocks can mean more K splits
     int s = 1;
-    for (int tn : {128, 256})
+    for (int tn : {128, 160, 256})
         for (int g : {64, 128}) {
             const int v = ds::splits_for(d, ff, g, (total_rows + tn - 1) / tn);
             s = v > s ? v : s;
@@ -545,7 +549,9 @@ static int grouped_ffn_impl(const void* xperm, const int32_t* offsets, int E, co
     // so its weights are dequantised once instead of once per 128-row block
     int max_rows = 0;
     for (int i = 0; i < E; ++i) max_rows = std::max(max_rows, offsets[i + 1] - offsets[i]);
-    const int TN = max_rows > 128 ? 256 : 128;
+    const int TN = max_rows > 160 ? 256 : (max_rows > 128 ? 160 : 128);
+    static const bool shrink = !(getenv("DS_K3_NEFF") && getenv("DS_K3_NEFF")[0] == '0');   // A/B runs
+    const int n_eff = (shrink && max_rows <= TN) ? std::max(16, (max_rows + 15) & ~15) : TN;
     int max_mb = 0, mb_total = 0;
     for (int i = 0; i < E; ++i) {
         const int r = offsets[i + 1] - offsets[i];
@@ -572,12 +578,13 @@ static int grouped_ffn_impl(const void* xperm, const int32_t* offsets, int E, co
     cudaStream_t st = as_stream(stream);
     // GEMM1: K = d, N = ff
     CUtensorMap map1, map2;
-    int rc = make_act_map(&map1, xperm, total_rows, d, TN);
+    int rc = make_act_map(&map1, xperm, total_rows, d, n_eff);
     if (rc) return rc;
+    a1.n_eff = a2.n_eff = n_eff;
     a1.K = d; a1.N = ff; a1.G = G; a1.kt_per_split = d / BK; a1.splits = 1;
     a1.total_rows = total_rows; a1.out = h;
     // GEMM2: K = ff, N = d, split-K with a deterministic reduction
-    rc = make_act_map(&map2, h, total_rows, ff, TN);
+    rc = make_act_map(&map2, h, total_rows, ff, n_eff);
     if (rc) return rc;
     const int splits = splits_for(d, ff, G, mb_total);
     const size_t need = (size_t)splits * total_rows * d * sizeof(float);
@@ -601,9 +608,11 @@ static int grouped_ffn_impl(const void* xperm, const int32_t* offsets, int E, co
         if (er != cudaSuccess) rc = cuda_status(er, "ds_w4_grouped_ffn: event");
     }
     if (!rc)
-        rc = TN == 256 ? launch_gemm<2, 256>(map1, a1, E, max_mb, st) : launch_gemm<2, 128>(map1, a1, E, max_mb, st);
+        rc = TN == 256 ? launch_gemm<2, 256>(map1, a1, E, max_mb, st)
+           : TN == 160 ? launch_gemm<2, 160>(map1, a1, E, max_mb, st) : launch_gemm<2, 128>(map1, a1, E, max_mb, st);
     if (!rc)
-        rc = TN == 256 ? launch_gemm<1, 256>(map2, a2, E, max_mb, st) : launch_gemm<1, 128>(map2, a2, E, max_mb, st);
+        rc = TN == 256 ? launch_gemm<1, 256>(map2, a2, E, max_mb, st)
+           : TN == 160 ? launch_gemm<1, 160>(map2, a2, E, max_mb, st) : launch_gemm<1, 128>(map2, a2, E, max_mb, st);
     if (!rc && splits > 1) {
         const size_t n = (size_t)total_rows * d;
         int grid = (int)((n + 255) / 256);
@@ -626,7 +635,7 @@ static int grouped_ffn_impl(const void* xperm, const int32_t* offsets, int E, co
 // order reduction when the tile count alone cannot fill the SMs).
 extern "C" size_t ds_w4_linear_workspace(int rows, int K, int N) {
     int s = 1;
-    for (int tn : {128, 256})
+    for (int tn : {128, 160, 256})
         for (int g : {64, 128}) {
             const int v = ds::splits_for(N, K, g, (rows + tn - 1) / tn);
             s = v > s ? v : s;
@@ -640,16 +649,17 @@ extern "C" int ds_w4_linear_gemm(const void* x, int rows, const ds_w4_linear* w,
     DS_CHECK_ARG(rows >= 0 && N % BM == 0 && K % BK == 0 && (G == 64 || G == 128) && K % G == 0,
                  "ds_w4_linear_gemm: need N %% 128 == 0, K %% 64 == 0, G in {64, 128}");
     if (rows == 0) return DS_OK;
-    const int TN = rows > 128 ? 256 : 128;
+    const int TN = rows > 160 ? 256 : (rows > 128 ? 160 : 128);
     const int mb = (rows + TN - 1) / TN;
     GemmArgs a{};
+    a.n_eff = mb == 1 ? std::max(16, (rows + 15) & ~15) : TN;
     a.row_start[0] = 0;
     a.rows[0] = rows;
     a.w[0][0] = W4Mat{w->codes, (const uint16_t*)w->scales, w->zeros};
     int rc = make_codes_map(&a.codes_map[0][0], w->codes, N, K);
     if (rc) return rc;
     CUtensorMap map;
-    rc = make_act_map(&map, x, rows, K, TN);
+    rc = make_act_map(&map, x, rows, K, a.n_eff);
     if (rc) return rc;
     const int splits = splits_for(N, K, G, mb);
     DS_CHECK_ARG((K / splits) / G + 2 <= kMaxGroupsPerCta, "ds_w4_linear_gemm: K / G too large");
@@ -663,7 +673,8 @@ extern "C" int ds_w4_linear_gemm(const void* x, int rows, const ds_w4_linear* w,
         a.out = workspace;
     }
     cudaStream_t st = as_stream(stream);
-    rc = TN == 256 ? launch_gemm<1, 256>(map, a, 1, mb, st) : launch_gemm<1, 128>(map, a, 1, mb, st);
+    rc = TN == 256 ? launch_gemm<1, 256>(map, a, 1, mb, st)
+       : TN == 160 ? launch_gemm<1, 160>(map, a, 1, mb, st) : launch_gemm<1, 128>(map, a, 1, mb, st);
     if (rc) return rc;
     if (splits > 1) {
         const size_t n = (size_t)rows * N;

@@ -50,9 +50,13 @@ a = ap.parse_args()
 res = json.loads(Path(a.out).read_text()) if Path(a.out).exists() else {}
 if a.k4:
     ls = launches(a.k4)
-    sw = first(ls, r"staged_mma_swiglu|staged_gemv_kernel<2|mma_gemv_kernel<2|swiglu_gemv")
-    dn = first(ls, r"staged_gemv_kernel<1|mma_gemv_kernel<1|down_gemv")
-    parts = [x for x in (sw, dn) if x]
+    fused = first(ls, r"expert_fused_v6")
+    if fused:                                    # K4 v6: one launch is one expert
+        parts = [fused]
+    else:
+        sw = first(ls, r"staged_mma_swiglu|staged_gemv_kernel<2|mma_gemv_kernel<2|swiglu_gemv")
+        dn = first(ls, r"staged_gemv_kernel<1|mma_gemv_kernel<1|down_gemv")
+        parts = [x for x in (sw, dn) if x]
     res["K4 w4_swiglu_gemv+down_gemv"] = {"bytes_per_unit": sum(x["dram_bytes"] for x in parts),
                                           "launches": parts, "source": a.k4}
 if a.k3:
