@@ -36,6 +36,10 @@ METRIC = "Mixtral-8x7B W4 e2e latency (TTFT, decode tok/s) at 15% expert residen
 UNIT = "ms/request (prefill 512 + decode 128, batch 1)"
 
 
+def unit_for(args) -> str:
+    return f"ms/request (prefill {args.prefill} + decode {args.decode}, batch 1)"
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -310,13 +314,13 @@ def cpu_reference_sample(shape, prefill: int, decode_sample: int = 2, threads: i
                       f"layer reuses layer 0's weights (same arithmetic)"}
 
 
-def cpu_baseline_entry(shape, prefill: int, decode: int) -> dict:
+def cpu_baseline_entry(shape, prefill: int, decode: int, unit: str = UNIT) -> dict:
     """cpu_baseline object: all host threads (the headline) plus a 1-thread
     decode arm."""
     cb = cpu_reference_sample(shape, prefill)
     one = cpu_reference_sample(shape, prefill, decode_sample=1, threads=1, do_prefill=False)
     v = cb["ttft_ms"] + decode * cb["decode_ms_per_token"]
-    return {"value": round(v, 1), "unit": UNIT, "cores": cb["cores"], "kind": "port", "sample": cb["sample"],
+    return {"value": round(v, 1), "unit": unit, "cores": cb["cores"], "kind": "port", "sample": cb["sample"],
             "cpu_model": cb["cpu_model"], "nproc": cb["nproc"], "ttft_ms": round(cb["ttft_ms"], 1),
             "decode_ms_per_token": round(cb["decode_ms_per_token"], 1), "timed_s": cb["timed_s"],
             "single_thread": {"cores": 1, "decode_ms_per_token": round(one["decode_ms_per_token"], 1),
@@ -418,7 +422,7 @@ def run_reference(args):
             walls.append(1e3 * w)
             samp = r
     v = statistics.median(vals)
-    line = {"impl": "reference", "metric": METRIC, "value": round(v, 1), "unit": UNIT, "n_gpus": 0,
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 1), "unit": unit_for(args), "n_gpus": 0,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(statistics.median(walls), 1),
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
@@ -427,9 +431,9 @@ def run_reference(args):
             "ttft_ms": round(samp["ttft_ms"], 1),
             "decode_tok_s": round(1e3 / samp["decode_ms_per_token"], 3),
             "value_from_sample": "ttft (measured, all layers) + decode tokens x measured ms/token of the sample",
-            "cpu_baseline": {"value": round(v, 1), "unit": UNIT, "cores": samp["cores"], "kind": "port",
+            "cpu_baseline": {"value": round(v, 1), "unit": unit_for(args), "cores": samp["cores"], "kind": "port",
                              "sample": samp["sample"], "cpu_model": samp["cpu_model"], "nproc": samp["nproc"]},
-            "e2e": {"value": round(v, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": round(v, 1), "unit": unit_for(args), "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
 
@@ -583,7 +587,7 @@ def run_ours(args):
     res_b = eng.resident_bytes()
     peak_dev = torch.cuda.max_memory_allocated(dev)
     line = {
-        "metric": METRIC, "value": round(ms_step, 1), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "metric": METRIC, "value": round(ms_step, 1), "unit": unit_for(args), "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 1), "higher_is_better": False,
         "scaling": "strong" if ep else "weak",
         "vs_baseline": None, "dtype": "bf16 activations, W4 (int4 g128) experts, f32 accumulate",
@@ -611,7 +615,7 @@ def run_ours(args):
         "roofline": kern["dominant"],
         "kernels": kern["all"],
         "gpu_launches": kern["launches"],
-        "e2e": {"value": round(e2e_ms, 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d_step),
+        "e2e": {"value": round(e2e_ms, 1), "unit": unit_for(args), "h2d_bytes_per_step": int(h2d_step),
                 "d2h_bytes_per_step": int(r0["d2h"])},
         "clocks": clk.summary(),
         "setup_s": round(setup_s, 1),
@@ -622,7 +626,7 @@ def run_ours(args):
     if not args.no_parity and rank == 0:
         line["parity"] = parity_leg(eng, args, shape, net, pop, aff, r0, one_step)
     if not args.no_cpu_baseline and ws == 1:
-        line["cpu_baseline"] = cpu_baseline_entry(shape, args.prefill, args.decode)
+        line["cpu_baseline"] = cpu_baseline_entry(shape, args.prefill, args.decode, unit_for(args))
     if args.also_22b and ws == 1 and shape.name == "mixtral-8x7b" and args.policy == "duoserve":
         # free this engine's device and pinned host memory, then BASELINE configs[2] in its own process
         st_ = eng.store

@@ -42,9 +42,11 @@ def _bits(x: torch.Tensor) -> np.ndarray:
 
 
 class TinyMixtralRef:
-    def __init__(self, shape, dense, seed: int):
-        """shape: ModelShape-like (attributes), dense: DenseWeights on CPU (bf16)."""
+    def __init__(self, shape, dense, seed: int, flash_p: bool = True):
+        """shape: ModelShape-like (attributes), dense: DenseWeights on CPU (bf16).
+        flash_p: emulate the fused attention kernels' bf16 probabilities."""
         self.s = shape
+        self.flash_p = flash_p
         self.W = dense
         self.seed = seed
         d, ff, G = shape.hidden, shape.ffn, shape.group_size
@@ -113,7 +115,16 @@ class TinyMixtralRef:
         n = Kx.shape[0]
         causal = torch.arange(n)[None, :] <= (torch.arange(T)[:, None] + self.pos)
         S = S.masked_fill(~causal[None], float("-inf"))
-        o = _bf(torch.einsum("hts,shd->thd", torch.softmax(S, -1), Vx)).reshape(T, -1)
+        if self.flash_p:
+            # the fused attention kernels' numerics: unnormalised probabilities
+            # exp(S - rowmax) rounded to bf16 for the P V product (f32
+            # accumulation), normalised by the f32 row sum afterwards
+            m = S.amax(-1, keepdim=True)
+            Pu = torch.exp(S - m)
+            o = torch.einsum("hts,shd->thd", _bf(Pu), Vx) / Pu.sum(-1).transpose(0, 1)[..., None]
+            o = _bf(o).reshape(T, -1)
+        else:
+            o = _bf(torch.einsum("hts,shd->thd", torch.softmax(S, -1), Vx)).reshape(T, -1)
         return _bf(h + o @ self._w(l, "wo", T).T)
 
     def gate(self, l, a):

@@ -131,6 +131,25 @@ def cache_log_decode_batch(paths_b, preds_b, L: int, policy: str = "duoserve", p
     return log, {"prefetch_hits": hits, "prefetch_misses": misses}
 
 
+def cache_log_ep_dispatch(prefill_paths_by_rank, decode_paths_by_rank, L: int, owned):
+    """Expert parallelism with token dispatch (engine.BatchEngine(ep=...),
+    ondemand): per layer visit the owner fetches the experts it owns that ANY
+    rank's tokens selected, ascending.  prefill_paths_by_rank[r] = that rank's
+    prefill token paths; decode_paths_by_rank[r][t][b] = its sequence b's path
+    at decode step t."""
+    own = set(owned)
+    log = []
+    for l in range(L):
+        sel = {e for paths in prefill_paths_by_rank for p in paths for e in p[l]}
+        log.append({"phase": "prefill", "layer": l, "fetch": _sorted(sel & own), "kind": "ep-dispatch"})
+    steps = len(decode_paths_by_rank[0])
+    for t in range(steps):
+        for l in range(L):
+            sel = {e for rk in decode_paths_by_rank for p in rk[t] for e in p[l]}
+            log.append({"phase": "decode", "token": t, "layer": l, "fetch": _sorted(sel & own), "kind": "ep-dispatch"})
+    return log
+
+
 # --------------------------------------------------------------------------
 # integer-ns timelines for the SPEC fixtures
 

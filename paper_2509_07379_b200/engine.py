@@ -1049,8 +1049,8 @@ class BatchEngine(Engine):
             raise ValueError("batch must be >= 1")
         if SchedulerPolicy(policy) in (SchedulerPolicy.DUOSERVE_ORACLE, SchedulerPolicy.PREFETCH_ALL):
             raise ValueError(f"BatchEngine serves 'duoserve' and 'ondemand' (got {policy!r})")
-        if kw.get("ep") is not None:
-            raise ValueError("BatchEngine: expert parallelism is single-sequence only")
+        if kw.get("ep") is not None and SchedulerPolicy(policy) is not SchedulerPolicy.ON_DEMAND:
+            raise ValueError("BatchEngine with expert parallelism (token dispatch) serves policy 'ondemand'")
         self.B = int(batch)
         self.max_prompt = int(max_prompt)
         super().__init__(shape, policy, max_seq=max_seq, max_prefill=self.B * self.max_prompt, **kw)
@@ -1096,7 +1096,10 @@ class BatchEngine(Engine):
         self._spec_fetch(0)
         for l in range(self.L):
             h = attention_block_batch(self.shape, self.W.layers[l], h, self.kv, l, 0, self.cos, self.sin)
-            hf, idx_host = self._moe_prefill(l, h.reshape(T, self.d), T)
+            if self.ep is not None:
+                hf, idx_host = self._moe_ep(l, "prefill", h.reshape(T, self.d), T)
+            else:
+                hf, idx_host = self._moe_prefill(l, h.reshape(T, self.d), T)
             h = hf.view(self.B, P, self.d)
             idx_all.append(idx_host)
         self.kv.len = P
@@ -1130,7 +1133,13 @@ class BatchEngine(Engine):
         for l in range(self.L):
             self.g_graphs[l].replay()                              # attention + norm + K1 gate (B rows)
             ops._count("ds_gate_topk")
-            h, rows = self._moe_decode_batch(l, self.g_h1, self.g_a2, self.g_h)
+            if self.ep is not None:
+                out, idx_host = self._moe_ep(l, "decode", self.g_h1, self.B, a=self.g_a2)
+                self.g_h.copy_(out)
+                h = self.g_h
+                rows = [tuple(int(e) for e in r) for r in idx_host.tolist()]
+            else:
+                h, rows = self._moe_decode_batch(l, self.g_h1, self.g_a2, self.g_h)
             for b in range(self.B):
                 paths[b].append(rows[b])
         self.kv.len = pos + 1
@@ -1150,6 +1159,54 @@ class BatchEngine(Engine):
         for _ in range(n_new - 1):
             out.append(self.decode_step())
         return out
+
+    def _moe_ep(self, l: int, phase: str, h, T: int, a=None):
+        """Expert parallelism with token dispatch (batch > 1):
+        this rank's T rows are routed here, dispatched to the expert owners
+        over all-to-all (ep.dispatch_combine), each owner fetches the experts
+        it received rows for (on demand, ascending, through its own slot ring
+        and copy stream) and runs them (K4 for <= 16 rows, K3 above), the
+        outputs come back and are combined in slot order.  Log per layer:
+        the owned experts fetched = (union of every rank's selections) ∩
+        owned (oracle: sim_ref.cache_log_ep_dispatch)."""
+        from .ep import dispatch_combine
+        sh = self.shape
+        if a is None:
+            a = rms_norm(h, self.W.layers[l]["ln2"], sh.rms_eps)
+            idx, w = self.p_idx[:T], self.p_w[:T]
+            ops.gate_topk(a, self.W.layers[l]["wg"], self.k, idx, w)
+            if self.p_paths is not None:
+                self.p_paths[:T, l].copy_(idx)
+        else:
+            idx, w = self.idx1, self.w1
+        idx_host = idx.cpu()
+        if self.capture is not None:
+            self.capture.append((phase, l, a.cpu(), idx_host.clone()))
+        ran = []
+
+        def ffn(e: int, rows: torch.Tensor) -> torch.Tensor:
+            n = rows.shape[0]
+            slot = self._next_ring_slot()
+            self.cache.load(slot, l, e)
+            st = self.cache.acquire(slot)
+            y = torch.zeros((n, self.d), dtype=torch.float32, device=self.device)
+            hb = torch.empty((n, self.ff), dtype=torch.bfloat16, device=self.device)
+            if n <= self.GEMV_ROWS:
+                ops.expert_gemv(rows.contiguous(), st, self.d, self.ff, self.G, hb, self.ones, 0, y)
+            else:
+                ws = torch.empty(max(ops.grouped_ffn_workspace(n, self.d, self.ff), 256), dtype=torch.uint8,
+                                 device=self.device)
+                ops.grouped_ffn(rows.contiguous(), [0, n], [st], self.d, self.ff, self.G, hb, y, ws)
+            self.cache.release(slot)
+            ran.append(e)
+            return y
+
+        out, _ = dispatch_combine(a, idx, w, h, self.ep, ffn, self.M)
+        rec = {"phase": phase, "layer": l, "fetch": sorted(ran), "kind": "ep-dispatch"}
+        if phase == "decode":
+            rec = {"phase": phase, "token": self.t_decode, "layer": l, "fetch": sorted(ran), "kind": "ep-dispatch"}
+        self.log.append(rec)
+        return out, (idx_host.numpy() if phase == "prefill" else idx_host)
 
     def _batch_ffn(self, e: int, off, st) -> None:
         lo, hi = off[e], off[e + 1]

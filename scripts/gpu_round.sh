@@ -24,17 +24,17 @@ for s in $STEPS; do
     kbench) log kbench; timeout 600 python scripts/kbench.py --iters 20 > gpurun_out/kbench.json 2> gpurun_out/kbench.err; log "kbench rc=$?";;
     launches)
       log launches
-      timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "timed/" \
+      DS_LAUNCH_GATE=0 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "timed/" \
         --csv --log-file gpurun_out/launches.csv \
         python bench.py --steps 1 --warmup 1 --decode 4 --warmup-decode 2 --no-cpu-baseline > gpurun_out/launches.log 2>&1
       log "launches rc=$?"
       python scripts/summarize_launches.py gpurun_out/launches.csv > gpurun_out/launches_summary.md 2>&1;;
     ncu)
       log ncu
-      timeout 900 ncu --set full --clock-control none --import-source on -k regex:'staged_gemv|swiglu_gemv|down_gemv' -s 4 -c 4 \
+      DS_LAUNCH_GATE=0 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'staged_gemv|swiglu_gemv|down_gemv' -s 4 -c 4 \
         -o gpurun_out/k4 -f python scripts/kbench.py --only k4 --iters 3 > gpurun_out/ncu_k4.log 2>&1
       log "ncu k4 rc=$?"
-      timeout 900 ncu --set full --clock-control none --import-source on -k regex:'w4_gemm' -s 4 -c 2 \
+      DS_LAUNCH_GATE=0 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'w4_gemm' -s 4 -c 2 \
         -o gpurun_out/k3 -f python scripts/kbench.py --only k3 --iters 3 > gpurun_out/ncu_k3.log 2>&1
       log "ncu k3 rc=$?";;
   esac

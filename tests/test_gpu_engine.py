@@ -78,10 +78,11 @@ def test_routing_bit_exact_teacher_forced(tiny):
     assert n == PREFILL * 4 + (DECODE - 1) * 4
 
 
-def test_logits_within_tolerance(tiny):
+@pytest.mark.parametrize("flash_p", [True, False])
+def test_logits_within_tolerance(tiny, flash_p):
     """Oracle replays the same tokens with the GPU's routing (teacher forcing)."""
     eng, shape = tiny["eng"], tiny["shape"]
-    ref = model_ref.TinyMixtralRef(shape, tiny["dense"], seed=3)
+    ref = model_ref.TinyMixtralRef(shape, tiny["dense"], seed=3, flash_p=flash_p)
     L = shape.num_layers
     pre_idx = [eng.paths_prefill[:, l, :] for l in range(L)]
     lg, _ = ref.forward(tiny["ids"].tolist(), decode=False, idx_override=pre_idx)
@@ -96,7 +97,8 @@ def test_logits_within_tolerance(tiny):
         g = tiny["logits"][t + 1]
         rels.append(((g - lg).norm() / lg.norm()).item())
         agree.append(int(torch.argmax(g)) == int(torch.argmax(lg)))
-    print("logit rel-L2 per step:", ["%.2e" % r for r in rels], "top1 agree", sum(agree), "/", len(agree))
+    print("flash_p", flash_p, "logit rel-L2 per step:", ["%.2e" % r for r in rels], "top1 agree", sum(agree), "/",
+          len(agree))
     assert max(rels) <= LOGIT_TOL, rels
     assert all(agree)
 

