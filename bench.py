@@ -519,6 +519,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         w2 = time.perf_counter()
         return {"ttft_ms": e0.elapsed_time(e1), "decode_ms": e1.elapsed_time(e2),
+                "host_wait_ms": {k_: round(1e3 * v_, 1) for k_, v_ in eng.host_wait.items()},
                 "e2e_wall_ms": 1e3 * (w2 - w0), "ttft_wall_ms": 1e3 * (w1 - w0),
                 "h2d_experts": eng.h2d_bytes() - c0, "tokens": toks,
                 "d2h": eng.d2h_bytes, "log": eng.log, "paths_prefill": eng.paths_prefill,
@@ -620,6 +621,7 @@ def run_ours(args):
         "clocks": clk.summary(),
         "setup_s": round(setup_s, 1),
         "predictor": {**eng.hit_summary(), "source": args.predictor,
+                      "host_wait_ms_per_request": r0.get("host_wait_ms"),
                       **({"preprocess": preprocess_summary(pre, shape)} if pre is not None else {})},
         "pinning": pin_info,
     }

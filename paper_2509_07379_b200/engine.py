@@ -555,6 +555,7 @@ class Engine:
         self._pa_queued = 0                   # prefetchall: layer visits queued on the copy stream
         self.hist.zero_()
         self.d2h_bytes = 0
+        self.host_wait = {"sync1": 0.0, "sync2": 0.0}     # host seconds blocked at sync points 1 / 2 (decode)
         if hasattr(self, "link"):
             self.cache.copy_stream.synchronize()
 
@@ -864,7 +865,9 @@ class Engine:
         use_pred = self.driver is not None
         if use_pred and l + 1 < self.L:
             self.driver.launch(self.hist, self.ev_gate, l + 1)     # predict stream, overlapped
+        t_w = time.perf_counter()
         link.wait_event(ev_idx)                                    # sync point 1: E_l on the host
+        self.host_wait["sync1"] += time.perf_counter() - t_w
         self.d2h_bytes += self.idx_host.nbytes + ((4 * self.k + 8 * self.M) if use_pred else 0)
         E = [int(e) for e in self.idx_host[0].tolist()]
         if self.capture is not None:
@@ -922,7 +925,9 @@ class Engine:
         self._record_moe("decode", l, h, a, out, self.idx_host, self.w1)
         # sync point 2: prediction for l+1 ready -> prefetch into the slots layer l-1 used
         if use_pred and l + 1 < self.L:
+            t_w = time.perf_counter()
             Pn, order = self.driver.result(link)
+            self.host_wait["sync2"] += time.perf_counter() - t_w
             cur = set(slot_of.values())
             free = [s_ for s_ in range(self.n_slots) if s_ not in cur][: self.k]
             pending = {}

@@ -56,3 +56,35 @@ def test_peak_memory_accounting(preset):
     if preset == "mixtral-8x7b":
         assert abs(peak[P.DUOSERVE] - 3.91e9) / 3.91e9 < 0.05
         assert peak[P.DUOSERVE] / cfg.total_param_bytes <= 0.16
+
+
+def test_batch_extension_reduces_to_single_sequence_and_unions():
+    """cache_log_decode_batch: B = 1 is exactly cache_log_decode; with B > 1
+    the gate set is the union of the sequences' selections, the prediction
+    the union of their predictions, refetch = gate - pred (hand-traced)."""
+    import numpy as np
+    from oracle import sim_ref
+    rng = np.random.default_rng(3)
+    L, M = 4, 8
+    paths = [tuple(tuple(sorted(rng.choice(M, 2, replace=False).tolist())) for _ in range(L)) for _ in range(5)]
+    preds = [[None] + [tuple(sorted(rng.choice(M, 2, replace=False).tolist())) for _ in range(L - 1)] for _ in paths]
+    one, c1 = sim_ref.cache_log_decode(paths, preds, L)
+    bat, cb = sim_ref.cache_log_decode_batch([[p] for p in paths], [[q] for q in preds], L)
+    assert bat == one and cb["prefetch_misses"] == c1["prefetch_misses"]
+    step = [((0, 1), (2, 5)), ((1, 3), (5, 6))]
+    pr = [[None, (2, 4)], [None, (6, 7)]]
+    log, cnt = sim_ref.cache_log_decode_batch([step], [pr], 2)
+    assert log[0] == {"phase": "decode", "token": 0, "layer": 0, "fetch": [0, 1, 3], "kind": "ondemand"}
+    assert log[1] == {"phase": "decode", "token": 0, "layer": 1, "pred": [2, 4, 6, 7], "gate": [2, 5, 6],
+                      "refetch": [5]}
+    assert cnt == {"prefetch_hits": 2, "prefetch_misses": 1}
+
+
+def test_ep_dispatch_rule_is_owned_part_of_the_union():
+    from oracle import sim_ref
+    pre = [[((0, 1), (2, 3))], [((4, 5), (3, 6))]]          # rank 0 / rank 1 prefill tokens
+    dec = [[[((1, 7), (0, 2))]], [[((2, 7), (5, 6))]]]        # one decode step, one sequence per rank
+    log0 = sim_ref.cache_log_ep_dispatch(pre, dec, 2, owned=[0, 2, 4, 6])
+    log1 = sim_ref.cache_log_ep_dispatch(pre, dec, 2, owned=[1, 3, 5, 7])
+    assert [r["fetch"] for r in log0] == [[0, 4], [2, 6], [2], [0, 2, 6]]
+    assert [r["fetch"] for r in log1] == [[1, 5], [3], [1, 7], [5]]
