@@ -1221,11 +1221,12 @@ static int staged_mma_launch(const __nv_bfloat16* x, W4Ptr a, W4Ptr b, int N, __
 namespace k4f {
 constexpr int kConsumers = 16;
 constexpr int kThreads = 32 * (kConsumers + 1);
-constexpr int RBA = 16, RBB = 8;
 constexpr int kSmemCap = 227 * 1024;
 
-template <int KA, int KB>
+template <int KA, int KB, int RBA_, int RBB_>
 struct Geo {
+    static constexpr int RBA = RBA_, RBB = RBB_;            // phase-A / phase-B tile rows
+    static constexpr int PARTS = kConsumers / RBB;          // phase B: K parts per row (one warp each)
     static constexpr int GPRA = KA / 128, CODEA = KA / 2, SCA = GPRA * 2;
     static constexpr int ZA = (RBA * GPRA / 2 + 32 + 15) & ~15;
     static constexpr int MATA = RBA * CODEA + RBA * SCA + ZA;
@@ -1235,7 +1236,7 @@ struct Geo {
     static constexpr int STAGEB = RBB * CODEB + RBB * SCB + ZB;
     static constexpr int SLOT = ((STAGEA > STAGEB ? STAGEA : STAGEB) + 127) & ~127;
     static constexpr int NCHB = KB / 32;                       // 32-code chunks of a W2 row
-    static constexpr int CPLB = NCHB / 2 / 32;                 // chunks per lane per K-half
+    static constexpr int CPLB = NCHB / PARTS / 32;             // chunks per lane per K part
     static constexpr int XA = KA * 2 + GPRA * 4;               // phase A: x + per-group sums
     static constexpr int XREG = ((XA > NCHB * 4 ? XA : NCHB * 4) + 127) & ~127;   // phase B: per-32 sums of h
     // phase B keeps h (KB bf16 = 64 B per 32-chunk) in shared memory: the x
@@ -1245,7 +1246,7 @@ struct Geo {
     static constexpr int HX_CH = (XREG - HX_OFF) / 64;                  // chunks in the x region
     static constexpr int HT_OFF = (STAGEB + 127) & ~127;
     static constexpr int HT_CH = (SLOT - HT_OFF) / 64;                  // chunks per slot tail
-    static constexpr int RED = 2 * kConsumers * 2 * 16 * 4 + 2 * RBB * 2 * 4;
+    static constexpr int RED = 2 * kConsumers * 2 * 16 * 4 + 2 * kConsumers * 4;
     static constexpr int FIXED = XREG + RED + 64;
     static constexpr int stages() {
         int n = (kSmemCap - FIXED) / (SLOT + 24);
@@ -1262,12 +1263,12 @@ __device__ unsigned g_k4f_bar[k4s::kTicketSlots];
 __device__ unsigned long long g_k4f_dbg[1024 * 8];
 __device__ unsigned g_k4f_exit[k4s::kTicketSlots];
 
-template <int KA, int KB>
+template <int KA, int KB, int RBA, int RBB>
 __global__ void __launch_bounds__(k4f::kThreads, 1) expert_fused_v6_kernel(
     const __nv_bfloat16* __restrict__ x, W4Ptr w1, W4Ptr w3, W4Ptr w2, int S, __nv_bfloat16* __restrict__ hout,
     const float* __restrict__ route_w, float* __restrict__ out, unsigned slot_id, int dbg) {
     using namespace ds::sm100;
-    using Gm = k4f::Geo<KA, KB>;
+    using Gm = k4f::Geo<KA, KB, RBA, RBB>;
     auto stamp = [&](int i) {
         if (dbg && threadIdx.x == 0) {
             unsigned long long t;
@@ -1277,18 +1278,19 @@ __global__ void __launch_bounds__(k4f::kThreads, 1) expert_fused_v6_kernel(
     };
     stamp(0);
     constexpr int GPRA = Gm::GPRA, GPRB = Gm::GPRB;
-    constexpr int TA = KB / k4f::RBA;                 // phase-A tiles: rows of W1 / W3 (N = ff = KB)
-    constexpr int TB = KA / k4f::RBB;                 // phase-B tiles: rows of W2 (N = d = KA)
+    constexpr int TA = KB / Gm::RBA;                 // phase-A tiles: rows of W1 / W3 (N = ff = KB)
+    constexpr int TB = KA / Gm::RBB;                 // phase-B tiles: rows of W2 (N = d = KA)
     constexpr int T = TA + TB;
     constexpr int GPW = GPRA / k4f::kConsumers;       // phase A: quantisation groups per warp
     static_assert(GPRA % k4f::kConsumers == 0, "phase A K split must be whole groups");
-    static_assert((Gm::NCHB / 2) % 32 == 0, "phase B K halves must be whole lane chunks");
+    static_assert((Gm::NCHB / Gm::PARTS) % 32 == 0, "phase B K parts must be whole lane chunks");
+    static_assert(RBA == 16 || RBA == 8, "phase A tiles: 16 rows, or 8 (half-used m16 MMA) for wide K");
     extern __shared__ __align__(128) uint8_t smem[];
     const __nv_bfloat16* xs = reinterpret_cast<const __nv_bfloat16*>(smem);
     float* xgs = reinterpret_cast<float*>(smem + KA * 2);          // phase A: sum of x per group
     float* hsum = reinterpret_cast<float*>(smem);                  // phase B: sum of h per 32-chunk (aliases x)
     float* red = reinterpret_cast<float*>(smem + Gm::XREG);        // [2][16 warps][2 mats][16 rows]
-    float* redb = red + 2 * k4f::kConsumers * 2 * 16;              // [2][8 rows][2 halves]
+    float* redb = red + 2 * k4f::kConsumers * 2 * 16;              // [2][RBB rows][PARTS]
     uint8_t* stages = smem + Gm::FIXED;
     uint64_t* full = reinterpret_cast<uint64_t*>(stages + (size_t)S * Gm::SLOT);
     uint64_t* empty = full + S;
@@ -1324,11 +1326,11 @@ __global__ void __launch_bounds__(k4f::kThreads, 1) expert_fused_v6_kernel(
                 if (pending >= TA && pending < T) {
                     // the next W2 tile is ours: pull it into L2 now, so its bulk copy (issued once a
                     // slot frees, typically after the phase barrier) hits L2
-                    const int rp = (pending - TA) * k4f::RBB;
+                    const int rp = (pending - TA) * Gm::RBB;
                     bulk_prefetch_l2(reinterpret_cast<const uint8_t*>(w2.codes) + (size_t)rp * Gm::CODEB,
-                                     k4f::RBB * Gm::CODEB);
+                                     Gm::RBB * Gm::CODEB);
                     bulk_prefetch_l2(reinterpret_cast<const uint8_t*>(w2.scales) + (size_t)rp * Gm::SCB,
-                                     k4f::RBB * Gm::SCB);
+                                     Gm::RBB * Gm::SCB);
                 }
             }
             if (t >= T || t < 0) {
@@ -1339,10 +1341,10 @@ __global__ void __launch_bounds__(k4f::kThreads, 1) expert_fused_v6_kernel(
             hdr[slot] = t;
             uint8_t* dst = stages + (size_t)slot * Gm::SLOT;
             if (t < TA) {
-                const int r0 = t * k4f::RBA;
+                const int r0 = t * Gm::RBA;
                 const uint32_t zb0 = ((uint32_t)(r0 * GPRA) >> 1) & ~15u;
-                const uint32_t zb1 = (((uint32_t)((r0 + k4f::RBA) * GPRA) >> 1) + 15u) & ~15u;
-                const uint32_t cb = k4f::RBA * Gm::CODEA, sb = k4f::RBA * Gm::SCA, zb = zb1 - zb0;
+                const uint32_t zb1 = (((uint32_t)((r0 + Gm::RBA) * GPRA) >> 1) + 15u) & ~15u;
+                const uint32_t cb = Gm::RBA * Gm::CODEA, sb = Gm::RBA * Gm::SCA, zb = zb1 - zb0;
                 mbar_expect_tx(&full[slot], 2 * (cb + sb + zb));
                 const W4Ptr W[2] = {w1, w3};
 #pragma unroll
@@ -1355,10 +1357,10 @@ __global__ void __launch_bounds__(k4f::kThreads, 1) expert_fused_v6_kernel(
                     bulk_load(md + cb + sb, W[m].zeros + zb0, zb, &full[slot], pol);
                 }
             } else {
-                const int r0 = (t - TA) * k4f::RBB;
+                const int r0 = (t - TA) * Gm::RBB;
                 const uint32_t zb0 = ((uint32_t)(r0 * GPRB) >> 1) & ~15u;
-                const uint32_t zb1 = (((uint32_t)((r0 + k4f::RBB) * GPRB) >> 1) + 15u) & ~15u;
-                const uint32_t cb = k4f::RBB * Gm::CODEB, sb = k4f::RBB * Gm::SCB, zb = zb1 - zb0;
+                const uint32_t zb1 = (((uint32_t)((r0 + Gm::RBB) * GPRB) >> 1) + 15u) & ~15u;
+                const uint32_t cb = Gm::RBB * Gm::CODEB, sb = Gm::RBB * Gm::SCB, zb = zb1 - zb0;
                 mbar_expect_tx(&full[slot], cb + sb + zb);
                 bulk_load(dst, reinterpret_cast<const uint8_t*>(w2.codes) + (size_t)r0 * Gm::CODEB, cb, &full[slot],
                           pol);
@@ -1405,7 +1407,7 @@ __global__ void __launch_bounds__(k4f::kThreads, 1) expert_fused_v6_kernel(
         const int t = hdr[slot];
         const uint8_t* base = stages + (size_t)slot * Gm::SLOT;
         if (t >= 0 && t < TA) {                                    // ---- phase A: SwiGLU tile
-            const int r0 = t * k4f::RBA;
+            const int r0 = t * Gm::RBA;
             const uint32_t zb0 = ((uint32_t)(r0 * GPRA) >> 1) & ~15u;
             float acc[2][2] = {};
 #pragma unroll
@@ -1420,8 +1422,10 @@ __global__ void __launch_bounds__(k4f::kThreads, 1) expert_fused_v6_kernel(
                 for (int m = 0; m < 2; ++m)
 #pragma unroll
                     for (int hh = 0; hh < 2; ++hh)
-                        c[m][hh] = *reinterpret_cast<const uint4*>(base + m * Gm::MATA + (g + 8 * hh) * Gm::CODEA +
-                                                                   (4 * j + tq) * 16);
+                        c[m][hh] = (hh == 0 || RBA == 16)
+                                       ? *reinterpret_cast<const uint4*>(base + m * Gm::MATA + (g + 8 * hh) * Gm::CODEA +
+                                                                          (4 * j + tq) * 16)
+                                       : make_uint4(0u, 0u, 0u, 0u);       // 8-row tile: MMA rows 8-15 unused
                 float dd[2][4] = {};
 #pragma unroll
                 for (int w = 0; w < 4; ++w) {
@@ -1443,12 +1447,12 @@ __global__ void __launch_bounds__(k4f::kThreads, 1) expert_fused_v6_kernel(
                 for (int m = 0; m < 2; ++m) {
                     const uint8_t* mb = base + m * Gm::MATA;
 #pragma unroll
-                    for (int hh = 0; hh < 2; ++hh) {
+                    for (int hh = 0; hh < (RBA == 16 ? 2 : 1); ++hh) {
                         const int row = g + 8 * hh;
-                        const uint16_t sv = reinterpret_cast<const uint16_t*>(mb + k4f::RBA * Gm::CODEA +
+                        const uint16_t sv = reinterpret_cast<const uint16_t*>(mb + Gm::RBA * Gm::CODEA +
                                                                               row * Gm::SCA)[j];
                         const uint32_t zn = (uint32_t)((r0 + row) * GPRA + j);
-                        const uint32_t zq = ((uint32_t)mb[k4f::RBA * (Gm::CODEA + Gm::SCA) + (zn >> 1) - zb0] >>
+                        const uint32_t zq = ((uint32_t)mb[Gm::RBA * (Gm::CODEA + Gm::SCA) + (zn >> 1) - zb0] >>
                                              ((zn & 1) << 2)) & 15u;
                         const float z128 = __uint_as_float(0x43000000u | (zq << 16));
                         const float sc = __uint_as_float((uint32_t)sv << 16);
@@ -1467,7 +1471,7 @@ __global__ void __launch_bounds__(k4f::kThreads, 1) expert_fused_v6_kernel(
                 }
             }
             asm volatile("bar.sync 2, %0;" ::"n"(32 * k4f::kConsumers) : "memory");
-            if (warp == 0 && lane < 16) {
+            if (warp == 0 && lane < RBA) {
                 float av = 0.f, bv = 0.f;
 #pragma unroll
                 for (int w = 0; w < k4f::kConsumers; ++w) {
@@ -1517,15 +1521,15 @@ __global__ void __launch_bounds__(k4f::kThreads, 1) expert_fused_v6_kernel(
         }
         if (t < 0) break;
         {                                                          // ---- phase B: down tile
-            const int r0 = (t - TA) * k4f::RBB;
-            const int r = warp & (k4f::RBB - 1), hf = warp / k4f::RBB;
+            const int r0 = (t - TA) * Gm::RBB;
+            const int r = warp % Gm::RBB, hf = warp / Gm::RBB;      // row of the tile, K part
             const int n = r0 + r;
             const uint32_t zb0 = ((uint32_t)(r0 * GPRB) >> 1) & ~15u;
             const float o_prev = (hf == 0 && lane == 0) ? out[n] : 0.f;   // in flight during the dot product
             float acc = 0.f;
 #pragma unroll
             for (int i = 0; i < Gm::CPLB; ++i) {
-                const int c = hf * (Gm::NCHB / 2) + lane + 32 * i;
+                const int c = hf * (Gm::NCHB / Gm::PARTS) + lane + 32 * i;
                 const int gq = c >> 2;
                 const uint4* hp = h_chunk(c);
                 uint4 xv[4];
@@ -1533,9 +1537,9 @@ __global__ void __launch_bounds__(k4f::kThreads, 1) expert_fused_v6_kernel(
                 for (int q = 0; q < 4; ++q) xv[q] = hp[q ^ ((c >> 1) & 3)];
                 const float xsm = hsum[c];
                 const uint4 c4 = *reinterpret_cast<const uint4*>(base + r * Gm::CODEB + c * 16);
-                const uint16_t sv = reinterpret_cast<const uint16_t*>(base + k4f::RBB * Gm::CODEB + r * Gm::SCB)[gq];
+                const uint16_t sv = reinterpret_cast<const uint16_t*>(base + Gm::RBB * Gm::CODEB + r * Gm::SCB)[gq];
                 const uint32_t zn = (uint32_t)(n * GPRB + gq);
-                const uint8_t zv = base[k4f::RBB * (Gm::CODEB + Gm::SCB) + (zn >> 1) - zb0];
+                const uint8_t zv = base[Gm::RBB * (Gm::CODEB + Gm::SCB) + (zn >> 1) - zb0];
                 const uint32_t cw[4] = {c4.x, c4.y, c4.z, c4.w};
                 float pp[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -1555,11 +1559,15 @@ __global__ void __launch_bounds__(k4f::kThreads, 1) expert_fused_v6_kernel(
             acc = warp_sum(acc);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[slot]);
-            float* rb = redb + (itb & 1) * k4f::RBB * 2;
-            if (lane == 0) rb[r * 2 + hf] = acc;
+            float* rb = redb + (itb & 1) * k4f::kConsumers;
+            if (lane == 0) rb[r * Gm::PARTS + hf] = acc;
             asm volatile("bar.sync 4, %0;" ::"n"(32 * k4f::kConsumers) : "memory");
-            if (hf == 0 && lane == 0)
-                out[n] = __fadd_rn(o_prev, __fmul_rn(route_w[0], rb[r * 2 + 0] + rb[r * 2 + 1]));
+            if (hf == 0 && lane == 0) {
+                float y = rb[r * Gm::PARTS];
+#pragma unroll
+                for (int q = 1; q < Gm::PARTS; ++q) y += rb[r * Gm::PARTS + q];   // fixed order
+                out[n] = __fadd_rn(o_prev, __fmul_rn(route_w[0], y));
+            }
             ++itb;
         }
     }
@@ -1575,10 +1583,10 @@ __global__ void __launch_bounds__(k4f::kThreads, 1) expert_fused_v6_kernel(
     }
 }
 
-template <int KA, int KB>
+template <int KA, int KB, int RBA, int RBB>
 static int expert_v6_launch(const __nv_bfloat16* x, const ds_w4_expert* e, __nv_bfloat16* h, const float* rw,
                             float* acc, cudaStream_t st) {
-    using Gm = k4f::Geo<KA, KB>;
+    using Gm = k4f::Geo<KA, KB, RBA, RBB>;
     constexpr int S = Gm::stages();
     if constexpr (S < 3 || !Gm::h_fits(S)) {
         return 1;
@@ -1586,7 +1594,7 @@ static int expert_v6_launch(const __nv_bfloat16* x, const ds_w4_expert* e, __nv_
         static bool init = false;
         const size_t smem = Gm::smem(S);
         if (!init) {
-            cudaFuncSetAttribute(expert_fused_v6_kernel<KA, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            cudaFuncSetAttribute(expert_fused_v6_kernel<KA, KB, RBA, RBB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem);
             init = true;
         }
@@ -1603,7 +1611,7 @@ static int expert_v6_launch(const __nv_bfloat16* x, const ds_w4_expert* e, __nv_
         cfg.numAttrs = coop ? 1 : 0;
         const unsigned slot_id = k4s_next_slot();
         static const int dbg = getenv("DS_K4_V6_TIMELINE") ? 1 : 0;
-        cudaError_t er = cudaLaunchKernelEx(&cfg, expert_fused_v6_kernel<KA, KB>, x, to_ptr(e->w1), to_ptr(e->w3),
+        cudaError_t er = cudaLaunchKernelEx(&cfg, expert_fused_v6_kernel<KA, KB, RBA, RBB>, x, to_ptr(e->w1), to_ptr(e->w3),
                                             to_ptr(e->w2), S, h, rw, acc, slot_id, dbg);
         return er == cudaSuccess ? DS_OK : cuda_status(er, "ds_w4_expert_gemv (v6 fused)");
     }
@@ -1617,7 +1625,8 @@ static int expert_v6(const void* x, int R, const ds_w4_expert* e, int d, int ff,
     if (!check_linear(e->w1) || !check_linear(e->w3) || !check_linear(e->w2)) return 1;
     const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x);
     __nv_bfloat16* hb = static_cast<__nv_bfloat16*>(h);
-    if (d == 4096 && ff == 14336) return expert_v6_launch<4096, 14336>(xb, e, hb, rw, acc, st);
+    if (d == 4096 && ff == 14336) return expert_v6_launch<4096, 14336, 16, 8>(xb, e, hb, rw, acc, st);   // 8x7B
+    if (d == 6144 && ff == 16384) return expert_v6_launch<6144, 16384, 8, 4>(xb, e, hb, rw, acc, st);    // 8x22B
     return 1;
 }
 

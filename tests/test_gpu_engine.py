@@ -20,7 +20,7 @@ from paper_2509_07379_b200.model import init_dense_weights
 pytestmark = pytest.mark.gpu
 
 PREFILL, DECODE = 64, 16
-LOGIT_TOL = 3e-2  # bf16 activations + flash-attention bf16 P; measured max 2.2e-2 on 16 steps
+LOGIT_TOL = 1e-2  # SURVEY App. A.3 bar; measured max 6.1e-3 (oracle with bf16 attention probabilities) / 8.1e-3 (f32 softmax), W4 attention
 
 
 def _bits(x):

@@ -202,7 +202,8 @@ def test_w4_grouped_ffn_tcgen05(d, ff, rows, cuda):
         assert rel2 < 5e-5, (i, rel2)           # f32 accumulation over K up to 16384
 
 
-def test_expert_gemv_and_timed_grouped_ffn_match_split_calls(cuda):
+@pytest.mark.parametrize("d,ff", [(4096, 14336), (6144, 16384)])
+def test_expert_gemv_and_timed_grouped_ffn_match_split_calls(cuda, d, ff):
     """ds_w4_expert_gemv (one call: the fused v6 launch at 8x7B shapes, else
     SwiGLU + PDL down; native timing events) gives the separate calls' h bit
     for bit and their output to f32 summation order (v6 splits the down
@@ -210,7 +211,7 @@ def test_expert_gemv_and_timed_grouped_ffn_match_split_calls(cuda):
     and records a positive span."""
     import torch
     from paper_2509_07379_b200 import ops
-    d, ff, G = 4096, 14336, 128
+    G = 128
     offs, total = _layout(d, ff, G)
     blob = torch.zeros(total, dtype=torch.uint8, device=cuda)
     _lib.call("ds_w4_generate", 11, 0, 2, d, ff, G, _lib.ptr(blob), _lib.stream_ptr())
