@@ -1626,7 +1626,10 @@ static int expert_v6(const void* x, int R, const ds_w4_expert* e, int d, int ff,
     const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x);
     __nv_bfloat16* hb = static_cast<__nv_bfloat16*>(h);
     if (d == 4096 && ff == 14336) return expert_v6_launch<4096, 14336, 16, 8>(xb, e, hb, rw, acc, st);   // 8x7B
-    if (d == 6144 && ff == 16384) return expert_v6_launch<6144, 16384, 8, 4>(xb, e, hb, rw, acc, st);    // 8x22B
+    // 8x22B (d = 6144): a 16-row W1/W3 tile leaves two ring slots, and the 8-row
+    // variant <6144, 16384, 8, 4> measured 55.7 us against 48.2 us for the v5
+    // PDL pair (profiles/r2/k4_v6_22b.json) -> v5 stays there
+    if (d == 6144 && ff == 16384 && getenv("DS_K4_V6_22B")) return expert_v6_launch<6144, 16384, 8, 4>(xb, e, hb, rw, acc, st);
     return 1;
 }
 

@@ -17,7 +17,7 @@ from paper_2509_07379_b200.config import load_shape  # noqa: E402
 
 _lib.load()
 dev = torch.device("cuda")
-sh = load_shape("mixtral-8x7b")
+sh = load_shape(sys.argv[1] if len(sys.argv) > 1 else "mixtral-8x7b")
 d, ff, G = sh.hidden, sh.ffn, sh.group_size
 _, blob = ops.expert_layout(d, ff, G)
 NB = 4
