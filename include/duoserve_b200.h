@@ -13,7 +13,7 @@
  *   - plain pointers and sizes only; device pointers are caller-owned
  *     (allocated by the caller, e.g. as torch tensors), "stream" is a
  *     cudaStream_t passed as void*; no entry point allocates device memory
- *     (the diagnostic DS_K4_TIMELINE / DS_K4_FUSED switches excepted);
+ *     (the diagnostic DS_K4_TIMELINE switch excepted);
  *   - return 0 on success, a positive cudaError_t on a CUDA failure, or a
  *     negative DS_ERR_* on invalid arguments; ds_last_error() returns the
  *     calling thread's last message;

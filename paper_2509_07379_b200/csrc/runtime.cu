@@ -37,7 +37,7 @@ GateState* gate_state() {
         const char* env = getenv("DS_LAUNCH_GATE");
         if (env && env[0] == '0') return;
         // the diagnostic K4 paths allocate / synchronise inside the launch call
-        if (getenv("DS_K4_TIMELINE") || (getenv("DS_K4_FUSED") && getenv("DS_K4_FUSED")[0] == '1')) return;
+        if (getenv("DS_K4_TIMELINE")) return;
         void* wf = nullptr;
         void* rf = nullptr;
         cudaDriverEntryPointQueryResult q1, q2;

@@ -764,59 +764,6 @@ inline int mma_gemv_warps(int NG, int nmat) {
     return S < 1 ? 1 : (S > 8 ? 8 : S);
 }
 
-// One expert's decode FFN (R = 1) in ONE cooperative launch: the SwiGLU GEMV
-// over the W1 / W3 rows, a grid barrier (h complete in L2), then the down GEMV
-// over the W2 rows — the same per-row code as the two-kernel path, one launch
-// and one ramp-up instead of two.  The barrier counter is monotonic across
-// launches (the host passes this launch's target), so no reset is needed.
-template <int G, int U1, int U2>
-__global__ void __launch_bounds__(kGemvThreads, 2) expert_gemv_fused_kernel(
-    const __nv_bfloat16* __restrict__ x, W4Ptr w1, W4Ptr w3, W4Ptr w2, int d, int ff,
-    __nv_bfloat16* __restrict__ h, const float* __restrict__ route_w, float* __restrict__ out,
-    unsigned long long* __restrict__ bar, unsigned long long bar_target) {
-    extern __shared__ __align__(16) uint32_t sm[];
-    const int lane = threadIdx.x & 31;
-    const int warps = gridDim.x * (blockDim.x >> 5);
-    const int w0 = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    {
-        uint32_t* xs = sm;
-        float* xsum = reinterpret_cast<float*>(sm + d / 2);
-        stage_x(x, 1, d, xs, xsum);
-        const W4Ptr W[2] = {w1, w3};
-        for (int n = w0; n < ff; n += warps) {
-            float acc[2][1];
-            gemv_row<1, 2, U1, G, false>(W, n, d, xs, xsum, acc);
-            if (lane == 0) {
-                const float av = acc[0][0], bv = acc[1][0];
-                h[n] = __float2bfloat16_rn(av / (1.0f + expf(-av)) * bv);
-            }
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();                                   // h of every warp of this CTA before the arrival
-        asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(bar) : "memory");
-        unsigned long long v;
-        do {
-            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory");
-        } while (v < bar_target);
-    }
-    __syncthreads();
-    {
-        uint32_t* xs = sm;
-        float* xsum = reinterpret_cast<float*>(sm + ff / 2);
-        stage_x<true>(h, 1, ff, xs, xsum);
-        const W4Ptr W[1] = {w2};
-        for (int n = w0; n < d; n += warps) {
-            float acc[1][1];
-            gemv_row<1, 1, U2, G, false>(W, n, ff, xs, xsum, acc);
-            if (lane == 0) {
-                float* o = out + n;
-                *o = __fadd_rn(*o, __fmul_rn(route_w[0], acc[0][0]));
-            }
-        }
-    }
-}
 
 __global__ void finalize_kernel(float* __restrict__ acc, const __nv_bfloat16* __restrict__ resid,
                                 size_t n, __nv_bfloat16* __restrict__ out) {
@@ -1876,64 +1823,6 @@ extern "C" int ds_w4_down_gemv(const void* h, int R, const ds_w4_expert* e, int 
     return DS_OK;
 }
 
-// Fused one-launch path for R = 1, G = 128 at the shapes with a compiled
-// (U1, U2) pair; returns 1 (not applicable / not enabled) to fall back to the
-// two PDL-chained launches.  DS_K4_FUSED=1 enables it (A/B runs).
-template <int U1, int U2>
-static int expert_fused_launch(const void* x, const ds_w4_expert* e, int d, int ff, void* h, const float* rw,
-                               float* acc, cudaStream_t st) {
-    auto fn = expert_gemv_fused_kernel<128, U1, U2>;
-    static int grid = 0;
-    const size_t smem = (size_t)(d > ff ? d : ff) * 2 + (size_t)((d > ff ? d : ff) / 32) * 4;
-    if (!grid) {
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-        int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kGemvThreads, smem);
-        grid = (per_sm < 1 ? 1 : (per_sm > 2 ? 2 : per_sm)) * num_sms();
-    }
-    // one monotonic barrier counter per stream (launches on a stream are ordered)
-    static std::mutex mu;
-    static std::map<cudaStream_t, std::pair<unsigned long long*, unsigned long long>> ctr;
-    unsigned long long* bar;
-    unsigned long long target;
-    {
-        std::lock_guard<std::mutex> lk(mu);
-        auto it = ctr.find(st);
-        if (it == ctr.end()) {
-            unsigned long long* p = nullptr;
-            cudaError_t er = cudaMalloc(&p, sizeof(unsigned long long));
-            if (er != cudaSuccess) return cuda_status(er, "ds_w4_expert_gemv: barrier");
-            er = cudaMemset(p, 0, sizeof(unsigned long long));
-            if (er != cudaSuccess) return cuda_status(er, "ds_w4_expert_gemv: barrier");
-            it = ctr.emplace(st, std::make_pair(p, 0ull)).first;
-        }
-        it->second.second += (unsigned long long)grid;
-        bar = it->second.first;
-        target = it->second.second;
-    }
-    const __nv_bfloat16* xb = (const __nv_bfloat16*)x;
-    __nv_bfloat16* hb = (__nv_bfloat16*)h;
-    W4Ptr p1 = to_ptr(e->w1), p3 = to_ptr(e->w3), p2 = to_ptr(e->w2);
-    void* args[] = {(void*)&xb, (void*)&p1, (void*)&p3, (void*)&p2, (void*)&d, (void*)&ff, (void*)&hb, (void*)&rw,
-                    (void*)&acc, (void*)&bar, (void*)&target};
-    cudaError_t er = cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(kGemvThreads), args, smem, st);
-    return cuda_status(er, "ds_w4_expert_gemv: fused launch");
-}
-
-static int expert_gemv_fused(const void* x, int R, const ds_w4_expert* e, int d, int ff, int G, void* h,
-                             const float* rw, float* acc, cudaStream_t st) {
-    // opt-in: measured 41.9 us per 8x7B expert against 37.8 us for the two
-    // launches chained by PDL (cooperative launch + grid barrier cost more)
-    static const bool on = getenv("DS_K4_FUSED") && getenv("DS_K4_FUSED")[0] == '1';
-    if (!on || R != 1 || G != 128 || !e || !check_linear(e->w1) || !check_linear(e->w3) || !check_linear(e->w2) ||
-        !x || !h || !rw || !acc)
-        return 1;
-    const int pl1 = (d / 32) % 32 == 0 ? (d / 32) / 32 : 0;    // 16-B chunks per lane (W1/W3 rows)
-    const int pl2 = (ff / 32) % 32 == 0 ? (ff / 32) / 32 : 0;  // (W2 rows)
-    if (pl1 == 4 && pl2 == 14) return expert_fused_launch<4, 7>(x, e, d, ff, h, rw, acc, st);   // 8x7B
-    if (pl1 == 6 && pl2 == 16) return expert_fused_launch<3, 8>(x, e, d, ff, h, rw, acc, st);   // 8x22B
-    return 1;
-}
 
 extern "C" int ds_w4_expert_gemv(const void* x, int R, const ds_w4_expert* e, int d, int ff, int G, void* h,
                                  const float* route_w, int route_stride, float* acc, void* ev_start, void* ev_end,
@@ -1949,7 +1838,6 @@ extern "C" int ds_w4_expert_gemv(const void* x, int R, const ds_w4_expert* e, in
         if (er != cudaSuccess) rc = cuda_status(er, "ds_w4_expert_gemv: event");
     }
     if (!rc) rc = expert_v6(x, R, e, d, ff, G, h, route_w, acc, st);
-    if (rc == 1) rc = expert_gemv_fused(x, R, e, d, ff, G, h, route_w, acc, st);
     if (rc == 1) {        // no fused variant for this shape: the two-kernel path
         rc = ds_w4_swiglu_gemv(x, R, e, d, ff, G, h, stream);
         if (!rc) rc = ds_w4_down_gemv(h, R, e, d, ff, G, route_w, route_stride, acc, stream);
