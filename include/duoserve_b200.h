@@ -220,6 +220,17 @@ int ds_w4_grouped_ffn(const void *xperm, const int32_t *offsets, int E, const ds
 int ds_w4_grouped_ffn_ev(const void *xperm, const int32_t *offsets, int E, const ds_w4_expert *experts,
                          int d, int ff, int G, void *h, float *y, void *workspace,
                          size_t workspace_bytes, void *ev_start, void *ev_end, void *stream);
+/* Same over arbitrary row segments of xperm / h / y: expert i owns rows
+ * [row_start[i], row_start[i] + rows[i]) (host arrays; segments need not be
+ * contiguous — e.g. the HBM-resident pinned experts of a layer in one launch);
+ * rows outside every segment are not written.  The workspace is sized for
+ * max_i(row_start[i] + rows[i]) rows.                                       */
+size_t ds_w4_grouped_ffn_seg_workspace(const int32_t *row_start, const int32_t *rows, int E, int d, int ff,
+                                       int G);
+int ds_w4_grouped_ffn_seg_ev(const void *xperm, const int32_t *row_start, const int32_t *rows, int E,
+                             const ds_w4_expert *experts, int d, int ff, int G, void *h, float *y,
+                             void *workspace, size_t workspace_bytes, void *ev_start, void *ev_end,
+                             void *stream);
 
 /* ========================================================================
  * K6 — host->device expert link (copy engine), native scheduler thread.

@@ -103,6 +103,9 @@ _SIGS = {
     "ds_debug_k4v6_timeline": (_I, [_P, _I]),
     "ds_h2d_tma_copy": (_I, [_P, _P, _SZ, _I, _P]),
     "ds_w4_grouped_ffn": (_I, [_P, C.POINTER(_I), _I, C.POINTER(W4Expert), _I, _I, _I, _P, _P, _P, _SZ, _P]),
+    "ds_w4_grouped_ffn_seg_workspace": (_SZ, [C.POINTER(_I), C.POINTER(_I), _I, _I, _I, _I]),
+    "ds_w4_grouped_ffn_seg_ev": (_I, [_P, C.POINTER(_I), C.POINTER(_I), _I, C.POINTER(W4Expert), _I, _I, _I, _P, _P,
+                                      _P, _SZ, _P, _P, _P]),
     "ds_w4_grouped_ffn_ev": (_I, [_P, C.POINTER(_I), _I, C.POINTER(W4Expert), _I, _I, _I, _P, _P, _P, _SZ, _P, _P,
                                   _P]),
 }

@@ -410,12 +410,13 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
     }
 }
 
+// y[i] = sum_s part[s * stride + i] for i < n, in split order (deterministic)
 __global__ void split_reduce_kernel(const float* __restrict__ part, int splits, size_t n,
-                                    float* __restrict__ y) {
+                                    float* __restrict__ y, size_t stride) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
          i += (size_t)gridDim.x * blockDim.x) {
         float acc = part[i];
-        for (int s = 1; s < splits; ++s) acc = __fadd_rn(acc, part[(size_t)s * n + i]);
+        for (int s = 1; s < splits; ++s) acc = __fadd_rn(acc, part[(size_t)s * stride + i]);
         y[i] = acc;
     }
 }
@@ -515,48 +516,94 @@ extern "C" size_t ds_w4_grouped_ffn_workspace(int total_rows, int d, int ff) {
 
 
 
-static int grouped_ffn_impl(const void* xperm, const int32_t* offsets, int E, const ds_w4_expert* experts, int d,
-                            int ff, int G, void* h, float* y, void* workspace, size_t workspace_bytes,
-                            void* ev_start, void* ev_end, void* stream);
+static int grouped_ffn_impl(const void* xperm, const int32_t* row_start, const int32_t* nrows, int E,
+                            const ds_w4_expert* experts, int d, int ff, int G, void* h, float* y, void* workspace,
+                            size_t workspace_bytes, void* ev_start, void* ev_end, void* stream);
+
+// contiguous segments [offsets[i], offsets[i+1]) -> (row_start, rows)
+static int offsets_to_segments(const int32_t* offsets, int E, int32_t* rs, int32_t* nr) {
+    DS_CHECK_ARG(offsets && E >= 1 && E <= kMaxExperts, "ds_w4_grouped_ffn: bad offsets / E");
+    for (int i = 0; i < E; ++i) {
+        DS_CHECK_ARG(offsets[i] >= 0 && offsets[i + 1] >= offsets[i], "ds_w4_grouped_ffn: offsets must be non-decreasing");
+        rs[i] = offsets[i];
+        nr[i] = offsets[i + 1] - offsets[i];
+    }
+    return DS_OK;
+}
 
 extern "C" int ds_w4_grouped_ffn(const void* xperm, const int32_t* offsets, int E,
                                  const ds_w4_expert* experts, int d, int ff, int G, void* h, float* y,
                                  void* workspace, size_t workspace_bytes, void* stream) {
-    return grouped_ffn_impl(xperm, offsets, E, experts, d, ff, G, h, y, workspace, workspace_bytes, nullptr,
-                            nullptr, stream);
+    int32_t rs[kMaxExperts], nr[kMaxExperts];
+    int rc = offsets_to_segments(offsets, E, rs, nr);
+    if (rc) return rc;
+    return grouped_ffn_impl(xperm, rs, nr, E, experts, d, ff, G, h, y, workspace, workspace_bytes, nullptr, nullptr,
+                            stream);
+}
+
+// Exact workspace bytes of one ds_w4_grouped_ffn_seg_ev call (same tile and
+// split choice as the launch).
+extern "C" size_t ds_w4_grouped_ffn_seg_workspace(const int32_t* row_start, const int32_t* rows, int E, int d,
+                                                  int ff, int G) {
+    if (!row_start || !rows || E < 1 || E > kMaxExperts) return 0;
+    int total = 0, max_rows = 0;
+    for (int i = 0; i < E; ++i) {
+        total = std::max(total, row_start[i] + rows[i]);
+        max_rows = std::max(max_rows, (int)rows[i]);
+    }
+    const int TN = max_rows > 160 ? 256 : (max_rows > 128 ? 160 : 128);
+    int mb_total = 0;
+    for (int i = 0; i < E; ++i) mb_total += (rows[i] + TN - 1) / TN;
+    const int splits = ds::splits_for(d, ff, G, mb_total);
+    return splits > 1 ? (size_t)splits * total * d * sizeof(float) : 0;
+}
+
+extern "C" int ds_w4_grouped_ffn_seg_ev(const void* xperm, const int32_t* row_start, const int32_t* rows, int E,
+                                        const ds_w4_expert* experts, int d, int ff, int G, void* h, float* y,
+                                        void* workspace, size_t workspace_bytes, void* ev_start, void* ev_end,
+                                        void* stream) {
+    DS_CHECK_ARG(row_start && rows, "ds_w4_grouped_ffn_seg_ev: NULL segments");
+    return grouped_ffn_impl(xperm, row_start, rows, E, experts, d, ff, G, h, y, workspace, workspace_bytes, ev_start,
+                            ev_end, stream);
 }
 
 extern "C" int ds_w4_grouped_ffn_ev(const void* xperm, const int32_t* offsets, int E,
                                     const ds_w4_expert* experts, int d, int ff, int G, void* h, float* y,
                                     void* workspace, size_t workspace_bytes, void* ev_start, void* ev_end,
                                     void* stream) {
-    return grouped_ffn_impl(xperm, offsets, E, experts, d, ff, G, h, y, workspace, workspace_bytes, ev_start,
-                            ev_end, stream);
+    int32_t rs[kMaxExperts], nr[kMaxExperts];
+    int rc = offsets_to_segments(offsets, E, rs, nr);
+    if (rc) return rc;
+    return grouped_ffn_impl(xperm, rs, nr, E, experts, d, ff, G, h, y, workspace, workspace_bytes, ev_start, ev_end,
+                            stream);
 }
 
-static int grouped_ffn_impl(const void* xperm, const int32_t* offsets, int E, const ds_w4_expert* experts, int d,
-                            int ff, int G, void* h, float* y, void* workspace, size_t workspace_bytes,
-                            void* ev_start, void* ev_end, void* stream) {
+static int grouped_ffn_impl(const void* xperm, const int32_t* row_start, const int32_t* nrows, int E,
+                            const ds_w4_expert* experts, int d, int ff, int G, void* h, float* y, void* workspace,
+                            size_t workspace_bytes, void* ev_start, void* ev_end, void* stream) {
     DS_CHECK_ARG(E >= 1 && E <= kMaxExperts, "ds_w4_grouped_ffn: 1 <= E <= %d", kMaxExperts);
     DS_CHECK_ARG(d % BM == 0 && ff % BM == 0 && d % BK == 0 && ff % BK == 0,
                  "ds_w4_grouped_ffn: d, ff must be multiples of 128");
     DS_CHECK_ARG(G == 64 || G == 128, "ds_w4_grouped_ffn: G must be 64 or 128");
     DS_CHECK_ARG(d / G <= kMaxGroupsPerCta, "ds_w4_grouped_ffn: d / G must be <= %d", kMaxGroupsPerCta);
-    DS_CHECK_ARG(xperm && offsets && experts && h && y, "ds_w4_grouped_ffn: NULL pointer");
-    const int total_rows = offsets[E];
+    DS_CHECK_ARG(xperm && row_start && nrows && experts && h && y, "ds_w4_grouped_ffn: NULL pointer");
+    int total_rows = 0;
+    for (int i = 0; i < E; ++i) {
+        DS_CHECK_ARG(row_start[i] >= 0 && nrows[i] >= 0, "ds_w4_grouped_ffn: negative segment");
+        total_rows = std::max(total_rows, row_start[i] + nrows[i]);
+    }
     GemmArgs a1{}, a2{};
     // token tile: 256 rows (UMMA N = 256) once an expert has more than 128 rows,
     // so its weights are dequantised once instead of once per 128-row block
     int max_rows = 0;
-    for (int i = 0; i < E; ++i) max_rows = std::max(max_rows, offsets[i + 1] - offsets[i]);
+    for (int i = 0; i < E; ++i) max_rows = std::max(max_rows, (int)nrows[i]);
     const int TN = max_rows > 160 ? 256 : (max_rows > 128 ? 160 : 128);
     static const bool shrink = !(getenv("DS_K3_NEFF") && getenv("DS_K3_NEFF")[0] == '0');   // A/B runs
     const int n_eff = (shrink && max_rows <= TN) ? std::max(16, (max_rows + 15) & ~15) : TN;
     int max_mb = 0, mb_total = 0;
     for (int i = 0; i < E; ++i) {
-        const int r = offsets[i + 1] - offsets[i];
-        DS_CHECK_ARG(r >= 0 && offsets[i] >= 0, "ds_w4_grouped_ffn: offsets must be non-decreasing");
-        a1.row_start[i] = a2.row_start[i] = offsets[i];
+        const int r = nrows[i];
+        a1.row_start[i] = a2.row_start[i] = row_start[i];
         a1.rows[i] = a2.rows[i] = r;
         const int mb = (r + TN - 1) / TN;
         max_mb = mb > max_mb ? mb : max_mb;
@@ -614,12 +661,19 @@ static int grouped_ffn_impl(const void* xperm, const int32_t* offsets, int E, co
         rc = TN == 256 ? launch_gemm<1, 256>(map2, a2, E, max_mb, st)
            : TN == 160 ? launch_gemm<1, 160>(map2, a2, E, max_mb, st) : launch_gemm<1, 128>(map2, a2, E, max_mb, st);
     if (!rc && splits > 1) {
-        const size_t n = (size_t)total_rows * d;
-        int grid = (int)((n + 255) / 256);
-        if (grid > 4 * num_sms()) grid = 4 * num_sms();
-        split_reduce_kernel<<<grid, 256, 0, st>>>(static_cast<const float*>(workspace), splits, n, y);
-        cudaError_t er = cudaGetLastError();
-        if (er != cudaSuccess) rc = cuda_status(er, "ds_w4_grouped_ffn: split reduce");
+        // per segment: rows outside every segment (other experts' rows of a
+        // shared buffer) are never written
+        const size_t stride = (size_t)total_rows * d;
+        for (int i = 0; i < E && !rc; ++i) {
+            if (nrows[i] == 0) continue;
+            const size_t n = (size_t)nrows[i] * d, o = (size_t)row_start[i] * d;
+            int grid = (int)((n + 255) / 256);
+            if (grid > 4 * num_sms()) grid = 4 * num_sms();
+            split_reduce_kernel<<<grid, 256, 0, st>>>(static_cast<const float*>(workspace) + o, splits, n, y + o,
+                                                      stride);
+            cudaError_t er = cudaGetLastError();
+            if (er != cudaSuccess) rc = cuda_status(er, "ds_w4_grouped_ffn: split reduce");
+        }
     }
     if (!rc && ev_end) {
         cudaError_t er = cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_end), st);
@@ -680,7 +734,7 @@ extern "C" int ds_w4_linear_gemm(const void* x, int rows, const ds_w4_linear* w,
         const size_t n = (size_t)rows * N;
         int grid = (int)((n + 255) / 256);
         if (grid > 4 * num_sms()) grid = 4 * num_sms();
-        split_reduce_kernel<<<grid, 256, 0, st>>>(static_cast<const float*>(workspace), splits, n, y);
+        split_reduce_kernel<<<grid, 256, 0, st>>>(static_cast<const float*>(workspace), splits, n, y, n);
         DS_LAUNCH_CHECK("ds_w4_linear_gemm: split reduce");
     }
     return DS_OK;

@@ -785,8 +785,7 @@ class Engine:
             plan += [(e, self._next_ring_slot(), False) for e in A if not (spec and e == spec[2])]
         self.log.append({"phase": "prefill", "layer": l, "fetch": [e for e, _, _ in plan], "activated": A_all,
                          **({"pinned": A_pin} if self.pinned else {})})
-        for e in A_pin:
-            self._prefill_ffn(e, None, off, st=self.pinned[(l, e)])
+        self._prefill_pinned(l, A_pin, off)
         # sliding window over the slot ring: the copy into a slot is queued only
         # after the compute that last used it has been queued (its free event)
         window = self.n_slots if self.policy is not SchedulerPolicy.ON_DEMAND else self.n_slots
@@ -819,6 +818,32 @@ class Engine:
             self.prof.add("K3 w4_grouped_ffn (tcgen05)", evs[0], evs[1], self.store.blob_bytes,
                           6.0 * (hi - lo) * self.d * self.ff)
 
+    def _prefill_pinned(self, l: int, A_pin, off) -> None:
+        """The layer's HBM-resident pinned experts in ONE grouped K3 launch
+        (their rows are segments of the permuted buffer)."""
+        self._prefill_group([e for e in A_pin if off[e + 1] > off[e]], off,
+                            lambda e: self.pinned[(l, e)])
+
+    def _prefill_group(self, es, off, struct_of) -> None:
+        """Experts `es` (all resident) in one grouped K3 launch over their row
+        segments; one launch per expert when the split-K workspace of the
+        grouped call would not fit the preallocated one."""
+        if not es:
+            return
+        segs = [(off[e], off[e + 1] - off[e]) for e in es]
+        if len(es) == 1 or len(es) > 16 or \
+                ops.grouped_ffn_segments_workspace(segs, self.d, self.ff, self.G) > self.p_ws.numel():
+            for e in es:
+                self._prefill_ffn(e, None, off, st=struct_of(e))
+            return
+        structs = [struct_of(e) for e in es]
+        evs = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) if self.prof else (None, None)
+        ops.grouped_ffn_segments(self.p_xperm, segs, structs, self.d, self.ff, self.G, self.p_h, self.p_y, self.p_ws,
+                                 *evs)
+        if self.prof:
+            self.prof.add("K3 w4_grouped_ffn (tcgen05)", evs[0], evs[1], len(es) * self.store.blob_bytes,
+                          6.0 * sum(r for _, r in segs) * self.d * self.ff)
+
     def _prefill_combine(self, h, T, w, idx):
         out = torch.empty_like(h)
         if self.ep is None:
@@ -833,8 +858,9 @@ class Engine:
     def _moe_prefill_all(self, l, h, T, A, A_all, off, w, idx, idx_host):
         """prefetchall: the whole layer was queued two visits ago; compute the activated experts."""
         self.log.append({"phase": "prefill", "layer": l, "fetch": list(self.owned), "activated": A_all})
-        for e in A:
-            self._prefill_ffn(e, self._pa_slot(self._pa_v, e), off)
+        # the whole bank is resident: the layer's activated experts in one grouped launch
+        self._prefill_group([e for e in A if off[e + 1] > off[e]], off,
+                            lambda e: self.cache.acquire(self._pa_slot(self._pa_v, e)))
         self._pa_done()
         out = self._prefill_combine(h, T, w, idx)
         self._record_moe("prefill", l, h, rms_norm(h, self.W.layers[l]["ln2"], self.shape.rms_eps), out, idx_host, w)

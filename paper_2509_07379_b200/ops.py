@@ -137,6 +137,27 @@ def combine_finalize(acc: torch.Tensor, resid: torch.Tensor, out: torch.Tensor) 
     _count("ds_combine_finalize")
 
 
+def grouped_ffn_segments(x: torch.Tensor, segments: list, experts: list, d: int, ff: int, G: int,
+                         h: torch.Tensor, y: torch.Tensor, ws: torch.Tensor, ev_start=None, ev_end=None) -> None:
+    """K3 over arbitrary row segments [(row_start, rows)] of x / h / y, one
+    expert per segment, in ONE grouped launch (e.g. a layer's pinned experts)."""
+    E = len(experts)
+    rs = (C.c_int * E)(*[int(a) for a, _ in segments])
+    nr = (C.c_int * E)(*[int(b) for _, b in segments])
+    arr = (_lib.W4Expert * E)(*experts)
+    evs = _native_events(ev_start, ev_end) if (ev_start is not None or ev_end is not None) else (None, None)
+    _lib.call("ds_w4_grouped_ffn_seg_ev", ptr(x), rs, nr, E, arr, d, ff, G, ptr(h), ptr(y), ptr(ws), ws.numel(),
+              evs[0], evs[1], stream_ptr())
+    _count("ds_w4_grouped_ffn", 3)
+
+
+def grouped_ffn_segments_workspace(segments: list, d: int, ff: int, G: int) -> int:
+    E = len(segments)
+    rs = (C.c_int * E)(*[int(a) for a, _ in segments])
+    nr = (C.c_int * E)(*[int(b) for _, b in segments])
+    return int(_lib.query("ds_w4_grouped_ffn_seg_workspace", rs, nr, E, d, ff, G))
+
+
 def grouped_ffn_workspace(rows: int, d: int, ff: int) -> int:
     return int(_lib.query("ds_w4_grouped_ffn_workspace", rows, d, ff))
 

@@ -308,3 +308,41 @@ def test_cache_check_matches_sim_ref_refetch_rule(cuda):
     for t in range(T):
         ref = log[2 * t + 1]["refetch"]
         assert [int(idx[t, j]) for j in range(k) if got[t] >> j & 1] == ref, t
+
+
+def test_grouped_ffn_segments_one_launch(cuda):
+    """ds_w4_grouped_ffn_seg_ev: three experts over NON-contiguous row
+    segments in one grouped launch (the engine's pinned experts of a layer)
+    match per-expert launches (h bit-exact where the token tile agrees, y to
+    f32 split order), and rows outside every segment are never written."""
+    import torch
+    from paper_2509_07379_b200 import ops
+    d, ff, G = 4096, 14336, 128
+    offs, total = _layout(d, ff, G)
+    E = 3
+    blobs = torch.zeros((E, total), dtype=torch.uint8, device=cuda)
+    for i in range(E):
+        _lib.call("ds_w4_generate", 31, 2, i, d, ff, G, _lib.ptr(blobs[i]), _lib.stream_ptr())
+    es = [_expert_struct(blobs[i], offs) for i in range(E)]
+    R = 400
+    segs = [(10, 37), (120, 150), (300, 90)]            # gaps between the segments
+    x = _rand_bf16((R, d), 1.0, torch.Generator().manual_seed(6)).to(cuda)
+    h = torch.full((R, ff), 7.0, dtype=torch.bfloat16, device=cuda)
+    y = torch.full((R, d), -3.0, device=cuda)
+    ws = torch.empty(max(ops.grouped_ffn_segments_workspace(segs, d, ff, G), 16), dtype=torch.uint8, device=cuda)
+    ops.grouped_ffn_segments(x, segs, es, d, ff, G, h, y, ws)
+    torch.cuda.synchronize()
+    inside = torch.zeros(R, dtype=torch.bool)
+    for i, (a, n) in enumerate(segs):
+        inside[a:a + n] = True
+        h1 = torch.empty((n, ff), dtype=torch.bfloat16, device=cuda)
+        y1 = torch.empty((n, d), device=cuda)
+        w1 = torch.empty(max(ops.grouped_ffn_workspace(n, d, ff), 16), dtype=torch.uint8, device=cuda)
+        ops.grouped_ffn(x[a:a + n], [0, n], [es[i]], d, ff, G, h1, y1, w1)
+        torch.cuda.synchronize()
+        hd = (h[a:a + n].float() - h1.float()).norm() / h1.float().norm()
+        assert hd.item() < 1e-3, (i, hd.item())          # bf16 h; a tile change moves the f32 sum order only
+        rel = ((y[a:a + n] - y1).norm() / y1.norm()).item()
+        assert rel < 1e-4, (i, rel)
+    out = ~inside.to(cuda)
+    assert bool((y[out] == -3.0).all()) and bool((h[out] == 7.0).all())
