@@ -519,6 +519,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         w2 = time.perf_counter()
         return {"ttft_ms": e0.elapsed_time(e1), "decode_ms": e1.elapsed_time(e2),
+                "floors": eng.streamed_bytes_floor(),
                 "host_wait_ms": {k_: round(1e3 * v_, 1) for k_, v_ in eng.host_wait.items()},
                 "e2e_wall_ms": 1e3 * (w2 - w0), "ttft_wall_ms": 1e3 * (w1 - w0),
                 "h2d_experts": eng.h2d_bytes() - c0, "tokens": toks,
@@ -610,6 +611,14 @@ def run_ours(args):
                  "frac": round(r0["h2d_experts"] / ((ttft + dec_ms) / 1e3) / 1e9 / link_gbs, 3),
                  "ttft_floor_ms": round(eng.prefill_bytes_floor() / link_gbs / 1e6, 1),
                  "decode_floor_ms_per_token": round(eng.decode_bytes_floor() / link_gbs / 1e6, 2),
+                 "pinned_aware_floor": {
+                     "ttft_ms": round(r0["floors"]["prefill_bytes"] / link_gbs / 1e6, 1),
+                     "decode_ms_per_token": round(r0["floors"]["decode_bytes_per_token"] / link_gbs / 1e6, 2),
+                     "request_ms": round((r0["floors"]["prefill_bytes"] + args.decode *
+                                          r0["floors"]["decode_bytes_per_token"]) / link_gbs / 1e6, 1),
+                     "frac_of_measured": round((r0["floors"]["prefill_bytes"] + args.decode *
+                                                r0["floors"]["decode_bytes_per_token"]) / link_gbs / 1e6 /
+                                               (r0["ttft_ms"] + r0["decode_ms"]), 3)},
                  "timeline": {k: (round(v, 4) if isinstance(v, float) else v) for k, v in timeline.items()},
                  "busy_gbs": round(timeline_bytes / (timeline["copy_busy_ms"] / 1e3) / 1e9, 2)
                  if timeline["copy_busy_ms"] else None},

@@ -1018,6 +1018,26 @@ class Engine:
         """L * k * expert bytes per token (perfect prediction)."""
         return self.L * self.k * self.store.blob_bytes
 
+    def streamed_bytes_floor(self) -> dict:
+        """Bytes any schedule must move over the link for the last request
+        given the pinned experts (they never cross the link): prefill
+        sum_l |A_l minus pinned|, decode per token sum_l |E_l minus pinned|,
+        times the expert bytes (this rank's experts under EP)."""
+        pre = dec = 0
+        n_tok = 0
+        for r in self.log:
+            pins = set(r.get("pinned", []))
+            if r["phase"] == "prefill":
+                pre += len([e for e in r["activated"] if e in self.owned_set and e not in pins])
+            elif "gate" in r:
+                dec += len([e for e in r["gate"] if e in self.owned_set and e not in pins])
+            elif r.get("kind") == "ondemand":
+                dec += len(r["fetch"])
+            if r["phase"] == "decode" and r["layer"] == 0:
+                n_tok += 1
+        b = self.store.blob_bytes
+        return {"prefill_bytes": pre * b, "decode_bytes_per_token": dec * b / max(n_tok, 1)}
+
     def hit_summary(self) -> dict:
         """Prediction counters over the decode log, counted like
         oracle/sim_ref.cache_log_decode: prediction and gate sets restricted to
