@@ -40,6 +40,16 @@ def unit_for(args) -> str:
     return f"ms/request (prefill {args.prefill} + decode {args.decode}, batch 1)"
 
 
+def workload_config(shape, args, n_requests: int = 1) -> dict:
+    """The workload both arms measure (identical dicts, so the reference arm's
+    line describes the same config); implementation details go to "setup"."""
+    return {"workload": f"{shape.name}-shaped W4 random-init, batch 1, prefill {args.prefill} + decode "
+                        f"{args.decode}",
+            "model": shape.name, "global_batch": n_requests, "seq_len": args.prefill + args.decode,
+            "prefill": args.prefill, "decode": args.decode,
+            "l2": "inputs > L2: every expert byte is streamed from pinned host memory per request"}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -426,8 +436,7 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(statistics.median(walls), 1),
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": f"{shape.name} W4 random-init, batch 1, prefill {args.prefill} + decode "
-                                   f"{args.decode}", "prefill": args.prefill, "decode": args.decode},
+            "config": workload_config(shape, args),
             "ttft_ms": round(samp["ttft_ms"], 1),
             "decode_tok_s": round(1e3 / samp["decode_ms_per_token"], 3),
             "value_from_sample": "ttft (measured, all layers) + decode tokens x measured ms/token of the sample",
@@ -594,13 +603,11 @@ def run_ours(args):
         "scaling": "strong" if ep else "weak",
         "vs_baseline": None, "dtype": "bf16 activations, W4 (int4 g128) experts, f32 accumulate",
         "data": "synthetic (random-init W4 experts from a counter-based generator, random prompt ids)",
-        "config": {"workload": f"{shape.name}-shaped W4, batch 1, prefill {args.prefill} + decode {args.decode}, "
-                               f"1 request per GPU, policy {args.policy}"
-                               f"{'' if args.no_cancel else ' + chunked cancellable prefetch'}",
-                   "model": shape.name, "global_batch": 1 if ep else ws, "seq_len": args.prefill + args.decode,
-                   "parallelism": (f"ep{ws}-{ep.combine}" if ep else f"replicas{ws}") if ws > 1 else "single-gpu",
-                   "expert_slots": eng.n_slots, "numa": numa_info,
-                   "l2": "inputs > L2: every expert byte is streamed from pinned host memory per request"},
+        "config": workload_config(shape, args, 1 if ep else ws),
+        "setup": {"serving": f"1 request per GPU, policy {args.policy}"
+                             f"{'' if args.no_cancel else ' + chunked cancellable prefetch'}",
+                  "parallelism": (f"ep{ws}-{ep.combine}" if ep else f"replicas{ws}") if ws > 1 else "single-gpu",
+                  "expert_slots": eng.n_slots, "numa": numa_info},
         "ttft_ms": round(ttft, 2), "decode_tok_s": round(args.decode / (dec_ms / 1e3), 3),
         "decode_ms_per_token": round(dec_ms / args.decode, 3),
         "residency": {"peak_device_bytes": int(peak_dev), "model_bytes": int(shape.total_bytes),
@@ -677,7 +684,7 @@ def run_22b_subprocess(args, timeout_s: int = 900) -> dict:
         return {"error": f"rc={r.returncode}", "stderr_tail": r.stderr[-600:]}
     d = json.loads(lines[-1])
     keep = ("value", "unit", "ttft_ms", "decode_tok_s", "decode_ms_per_token", "residency", "link", "roofline",
-            "predictor", "pinning", "parity", "clocks", "config", "e2e")
+            "predictor", "pinning", "parity", "clocks", "config", "setup", "e2e")
     out = {k: d[k] for k in keep if k in d}
     out["command"] = " ".join(cmd[1:])
     out["wall_s"] = round(time.time() - t0, 1)
