@@ -1535,7 +1535,7 @@ static int expert_v6_launch(const __nv_bfloat16* x, const ds_w4_expert* e, __nv_
                             float* acc, cudaStream_t st) {
     using Gm = k4f::Geo<KA, KB, RBA, RBB>;
     constexpr int S = Gm::stages();
-    if constexpr (S < 3 || !Gm::h_fits(S)) {
+    if constexpr (S < 2 || !Gm::h_fits(S)) {
         return 1;
     } else {
         static bool init = false;
@@ -1576,7 +1576,10 @@ static int expert_v6(const void* x, int R, const ds_w4_expert* e, int d, int ff,
     // 8x22B (d = 6144): a 16-row W1/W3 tile leaves two ring slots, and the 8-row
     // variant <6144, 16384, 8, 4> measured 55.7 us against 48.2 us for the v5
     // PDL pair (profiles/r2/k4_v6_22b.json) -> v5 stays there
-    if (d == 6144 && ff == 16384 && getenv("DS_K4_V6_22B")) return expert_v6_launch<6144, 16384, 8, 4>(xb, e, hb, rw, acc, st);
+    if (d == 6144 && ff == 16384 && getenv("DS_K4_V6_22B")) {
+        if (getenv("DS_K4_V6_22B")[0] == '8') return expert_v6_launch<6144, 16384, 8, 4>(xb, e, hb, rw, acc, st);
+        return expert_v6_launch<6144, 16384, 16, 8>(xb, e, hb, rw, acc, st);     // two ring slots
+    }
     return 1;
 }
 
