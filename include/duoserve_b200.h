@@ -267,6 +267,12 @@ int ds_link_trace(ds_link *link, int enable);
 int ds_link_trace_read(ds_link *link, void *ref_event, float *start_ms, float *end_ms, size_t max_spans,
                        size_t *n_out);
 
+/* L2 residency for one stream's kernels: a persisting access-policy window
+ * over [base, base + bytes) (the predictor's f64 weights, so the streaming
+ * expert kernels do not evict them between calls); raises the device's
+ * persisting set-aside as needed. */
+int ds_l2_persist_window(void *stream, const void *base, size_t bytes, float hit_ratio);
+
 /* Diagnostics: per-CTA %globaltimer stamps (ns; [n_ctas][8]: entry, phase A
  * consumed, grid barrier passed, h staged, exit) of the last fused K4 v6
  * launch made with DS_K4_V6_TIMELINE=1 in the environment. */

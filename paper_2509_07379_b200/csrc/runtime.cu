@@ -151,3 +151,34 @@ extern "C" int ds_device_info(int* num_sms_out, int* is_sm100) {
     if (is_sm100) *is_sm100 = (major == 10 && minor == 0) ? 1 : 0;
     return DS_OK;
 }
+
+// Keep a buffer resident in L2 for the kernels of one stream: a persisting
+// access-policy window (hit ratio `hit_ratio`) over [base, base + bytes), with
+// the device's persisting L2 set-aside raised to cover it (capped by the
+// device maximum).  Used for the predictor's 23.9 MB of f64 weights, which
+// the streaming expert kernels would otherwise evict between calls.
+extern "C" int ds_l2_persist_window(void* stream, const void* base, size_t bytes, float hit_ratio) {
+    DS_CHECK_ARG(base && bytes > 0 && hit_ratio > 0.f && hit_ratio <= 1.f, "ds_l2_persist_window: bad arguments");
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return ds::cuda_status(e, "ds_l2_persist_window: device");
+    int max_persist = 0, max_window = 0;
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+    if (max_persist <= 0 || max_window <= 0) return ds::fail(DS_ERR_UNSUPPORTED, "ds_l2_persist_window: no L2 persistence");
+    size_t want = bytes < (size_t)max_persist ? bytes : (size_t)max_persist;
+    size_t cur = 0;
+    cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+    if (cur < want) {
+        e = cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+        if (e != cudaSuccess) return ds::cuda_status(e, "ds_l2_persist_window: set-aside");
+    }
+    cudaStreamAttrValue v = {};
+    v.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+    v.accessPolicyWindow.num_bytes = bytes < (size_t)max_window ? bytes : (size_t)max_window;
+    v.accessPolicyWindow.hitRatio = hit_ratio;
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    e = cudaStreamSetAttribute(ds::as_stream(stream), cudaStreamAttributeAccessPolicyWindow, &v);
+    return ds::cuda_status(e, "ds_l2_persist_window: stream window");
+}

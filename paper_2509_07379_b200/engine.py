@@ -360,13 +360,33 @@ class MLPDriver:
         self.sets = None                 # per-sequence predicted sets of the last result()
         self.done = torch.cuda.Event()
         self.nbytes = self.dev.nbytes + self.stats.pop.nbytes + self.stats.aff.nbytes
+        self.prof = None                 # KernelProfiler (set by the engine when profiling)
+        import os
+        # opt-in: a persisting L2 window over the 23.9 MB of weights measured no
+        # gain (K5 in the loop 43.7 vs 44.5 us: bound by its 7 dependent layers,
+        # not by bytes; profiles/r2/README.md)
+        self.l2_persist = os.environ.get("DS_K5_L2PERSIST", "0") == "1"
+        if self.l2_persist:              # the weights stay in L2 between the per-layer calls
+            from . import _lib
+            import ctypes as C
+            try:
+                _lib.call("ds_l2_persist_window", C.c_void_p(self.stream.cuda_stream),
+                          C.c_void_p(self.dev.packed.data_ptr()), self.dev.packed.numel() * 8, 1.0)
+            except Exception:
+                self.l2_persist = False
 
     def launch(self, hist: torch.Tensor, after: torch.cuda.Event, target_layer: int) -> None:
         with torch.cuda.stream(self.stream):
             self.stream.wait_event(after)
+            if self.prof is not None:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(self.stream)
             self.dev.predict_state(hist, self.targets[target_layer], self.stats.pop, self.stats.aff, self.L,
                                    self.M, self.k, self.mode, self.k, out=self.out, probs=self.probs,
                                    stream=self.stream)
+            if self.prof is not None:
+                e1.record(self.stream)
+                self.prof.add("K5 predictor (fused f64 MLP)", e0, e1, self.dev.nbytes)
             self.host_out.copy_(self.out, non_blocking=True)
             self.host_probs.copy_(self.probs, non_blocking=True)
             self.done.record(self.stream)
@@ -572,6 +592,8 @@ class Engine:
 
     def enable_profile(self) -> "KernelProfiler":
         self.prof = KernelProfiler()
+        if isinstance(self.driver, MLPDriver):
+            self.driver.prof = self.prof
         return self.prof
 
     @torch.no_grad()
