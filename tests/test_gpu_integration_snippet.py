@@ -41,15 +41,19 @@ def test_integration_snippet_predicts_reference_sets(cuda, tmp_path):
     saved = {k: sys.modules.get(k) for k in ("duoserve", "duoserve.predictor")}
     sys.modules["duoserve"], sys.modules["duoserve.predictor"] = pkg, pred
     try:
-        src = _snippet().replace('C.CDLL("libduoserve_sm100.so")', f'C.CDLL("{_lib.LIB_PATH}")')
-        ns = {}
-        exec(compile(src, "INTEGRATION.md:_b200.py", "exec"), ns)
+        _run_snippet(tmp_path)
     finally:
         for k, v in saved.items():
             if v is None:
                 sys.modules.pop(k, None)
             else:
                 sys.modules[k] = v
+
+
+def _run_snippet(tmp_path):
+    src = _snippet().replace('C.CDLL("libduoserve_sm100.so")', f'C.CDLL("{_lib.LIB_PATH}")')
+    ns = {}
+    exec(compile(src, "INTEGRATION.md:_b200.py", "exec"), ns)
     cfg, _ = C.load_preset("tiny-4x8")
     ds = T.generate_traces(T.default_generator_params(4, 8, 0.8, seed=7), cfg, 6, 8, 8)
     pop, aff = S.build_popularity(ds), S.build_affinity(ds)
