@@ -277,6 +277,9 @@ int ds_l2_persist_window(void *stream, const void *base, size_t bytes, float hit
  * consumed, grid barrier passed, h staged, exit) of the last fused K4 v6
  * launch made with DS_K4_V6_TIMELINE=1 in the environment. */
 int ds_debug_k4v6_timeline(unsigned long long *out, int n_ctas);
+/* Same for K3 with DS_K3_TIMELINE=1 (nmat 2: GEMM1, 1: GEMM2): entry, scales
+ * staged, first MMA issued, last MMA issued, accumulators ready, exit. */
+int ds_debug_k3_timeline(unsigned long long *out, int nmat, int n_ctas);
 
 /* SM-driven host->HBM copy: `ctas` CTAs stream `bytes` from mapped pinned host
  * memory (cudaHostAlloc / cudaHostRegister, UVA) over PCIe with 16-byte loads

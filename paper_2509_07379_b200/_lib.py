@@ -101,6 +101,7 @@ _SIGS = {
     "ds_link_trace_read": (_I, [_P, _P, C.POINTER(C.c_float), C.POINTER(C.c_float), _SZ, C.POINTER(_SZ)]),
     "ds_h2d_sm_copy": (_I, [_P, _P, _SZ, _I, _P]),
     "ds_debug_k4v6_timeline": (_I, [_P, _I]),
+    "ds_debug_k3_timeline": (_I, [_P, _I, _I]),
     "ds_l2_persist_window": (_I, [_P, _P, _SZ, C.c_float]),
     "ds_h2d_tma_copy": (_I, [_P, _P, _SZ, _I, _P]),
     "ds_w4_grouped_ffn": (_I, [_P, C.POINTER(_I), _I, C.POINTER(W4Expert), _I, _I, _I, _P, _P, _P, _SZ, _P]),

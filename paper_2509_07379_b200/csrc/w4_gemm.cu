@@ -57,6 +57,8 @@ struct GemmArgs {
     CUtensorMap codes_map[kMaxExperts][2];   // [N, K/2] u8 tiles {CK * 32 B, 128 rows}
     int K, N, G;
     int kt_per_split;   // k-tiles (of BK) per split
+    int diag;           // diagnostics only (DS_K3_DIAG): 1 = no MMAs, 2 = no dequant, 3 = no activation
+                        // loads, 4 = no code loads (results invalid)
     int n_eff;          // UMMA N actually issued (multiple of 16, <= TN): the token rows of a single
                         // m-block rounded up to 16, so a 151-row expert costs N = 160, not 256
     int splits;
@@ -128,14 +130,16 @@ __device__ __forceinline__ void dequant32_regs(const uint4 c, uint32_t zz, uint3
 template <int NMAT, int TN>
 bool plan_smem(GemmArgs& a) {
     using S = Smem<NMAT, TN>;
-    const int ng = (a.kt_per_split * BK + a.G - 1) / a.G + 1;        // groups one CTA can touch
-    const int sc = NMAT * BM * ng * 2, z = NMAT * BM * ng;
+    // the n-block's scales and (packed) zero nibbles of WHOLE weight rows are
+    // bulk-copied once per CTA: 128 contiguous rows of each matrix
+    const int gpr = a.K / a.G;
+    const int sc = NMAT * BM * gpr * 2, z = NMAT * BM * gpr / 2;
     const int fixed = S::C_OFF + ((sc + 15) & ~15) + ((z + 15) & ~15) + S::kBarBytes;
     int cs = (S::kBudget - fixed) / S::C_STAGE;
     if (cs > S::kMaxCS) cs = S::kMaxCS;
-    if (cs < 2 || ng > kMaxGroupsPerCta) return false;
+    if (cs < 2) return false;      // BM * gpr / 2 = 64 gpr bytes: a multiple of 16 for any gpr
     a.code_stages = cs;
-    a.ng_stride = ng;
+    a.ng_stride = gpr;
     a.sc_off = S::C_OFF + cs * S::C_STAGE;
     a.z_off = a.sc_off + ((sc + 15) & ~15);
     a.bar_off = (a.z_off + ((z + 15) & ~15) + 7) & ~7;
@@ -168,6 +172,19 @@ __device__ __forceinline__ void dequant32(const uint4 c, uint32_t zz, uint32_t s
     }
 }
 
+// diagnostics (DS_K3_TIMELINE=1 sets args.diag = 8): per-CTA %globaltimer
+// stamps [NMAT - 1][cta][8]: 0 entry, 1 scales staged, 2 first MMA issued,
+// 3 last MMA issued, 4 accumulators ready, 5 exit
+__device__ unsigned long long g_k3_dbg[2][1024][8];
+__device__ __forceinline__ void k3_stamp(int diag, int nmat, int slot) {
+    if (diag != 8) return;
+    const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    if (cta >= 1024) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_k3_dbg[nmat - 1][cta][slot] = t;
+}
+
 template <int NMAT, int TN>
 __global__ void __launch_bounds__(kThreads, 1)
 w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constant__ GemmArgs args) {
@@ -187,7 +204,8 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
     uint64_t* a_full = b_empty + BS;
     uint64_t* a_empty = a_full + AS;
     uint64_t* tmem_full = a_empty + AS;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+    uint64_t* s_full = tmem_full + 1;                 // the n-block's scales / zeros staged
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 1);
 
     const int e = blockIdx.z;
     const int rows = args.rows[e];
@@ -207,10 +225,12 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
         for (int s = 0; s < BS; ++s) { mbar_init(&b_full[s], 1); mbar_init(&b_empty[s], 1); }
         for (int s = 0; s < AS; ++s) { mbar_init(&a_full[s], kGroupThreads); mbar_init(&a_empty[s], 1); }
         mbar_init(tmem_full, 1);
+        mbar_init(s_full, 1);
         fence_mbar_init();
         tma_prefetch_desc(&act_map);
         for (int j = 0; j < NMAT; ++j) tma_prefetch_desc(&args.codes_map[e][j]);
     }
+    if (threadIdx.x == 0) k3_stamp(args.diag, NMAT, 0);
     if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
     tc_fence_before();
     __syncthreads();
@@ -220,10 +240,22 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
     if (warp == 0) {
         // ---------------------------------------------- code producer (HBM)
         if (lane == 0) {
+            {   // scales + packed zero nibbles of the block's 128 weight rows (whole rows, contiguous)
+                const int gpr = args.K / args.G;
+                const uint32_t sb = BM * gpr * 2, zb = BM * gpr / 2;
+                mbar_expect_tx(s_full, NMAT * (sb + zb));
+                const uint64_t pol = l2_evict_first_policy();
+#pragma unroll
+                for (int m = 0; m < NMAT; ++m) {
+                    bulk_load(smem + args.sc_off + m * sb, args.w[e][m].scales + (size_t)n0 * gpr, sb, s_full, pol);
+                    bulk_load(smem + args.z_off + m * zb, args.w[e][m].zeros + (size_t)n0 * gpr / 2, zb, s_full, pol);
+                }
+            }
             for (int j = 0; j < NCS; ++j) {
                 const int s = j % CS;
                 if (j >= CS) mbar_wait(&c_empty[s], ((j / CS) - 1) & 1);
                 uint8_t* c_tile = smem + S::C_OFF + s * S::C_STAGE;
+                if (args.diag == 4) { mbar_arrive(&c_full[s]); continue; }
                 mbar_expect_tx(&c_full[s], S::C_STAGE);
 #pragma unroll
                 for (int m = 0; m < NMAT; ++m)
@@ -238,6 +270,7 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
             for (int kt = 0; kt < KT; ++kt) {
                 const int s = kt % BS;
                 if (kt >= BS) mbar_wait(&b_empty[s], ((kt / BS) - 1) & 1);
+                if (args.diag == 3) { mbar_arrive(&b_full[s]); continue; }
                 mbar_expect_tx(&b_full[s], (uint32_t)args.n_eff * 128u);
                 tma_load_2d(smem + S::B_OFF + s * S::B_STAGE, &act_map, &b_full[s], (kt0 + kt) * BK, row_coord);
             }
@@ -255,6 +288,7 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
                 const uint64_t bdesc = umma_desc_sw128(smem_u32(smem + S::B_OFF + sb * S::B_STAGE));
 #pragma unroll
                 for (int kk = 0; kk < BK / UK; ++kk) {
+                    if (args.diag == 1) break;
 #pragma unroll
                     for (int j = 0; j < NMAT; ++j) {
                         if constexpr (S::A_TMEM) {
@@ -272,7 +306,9 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
                 }
                 mma_commit(&a_empty[sa]);
                 mma_commit(&b_empty[sb]);
+                if (kt == 0) k3_stamp(args.diag, NMAT, 2);
             }
+            k3_stamp(args.diag, NMAT, 3);
             mma_commit(tmem_full);
         }
     } else {
@@ -290,41 +326,11 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
         const int g0 = kt0 * BK / G;             // first group touching this CTA's k-range
         const int ng = ((kt0 + KT) * BK + G - 1) / G - g0;   // groups touched (<= kMaxGroupsPerCta)
         const int gshift = G == 128 ? 7 : 6;                 // G is 64 or 128 (checked on the host)
-        const W4Mat* W = args.w[e];
-        uint16_t* sc_s = reinterpret_cast<uint16_t*>(smem + args.sc_off);
-        uint8_t* z_s = smem + args.z_off;
-        const int ngs = args.ng_stride;
-        // stage the n-block's scales and zeros for the whole k-range once;
-        // batches of 8 independent loads per thread are issued before any
-        // store, so the prologue costs a few memory latencies, not one per element
-        {
-            const int total = NMAT * BM * ng;
-            constexpr int B8 = 8;
-            for (int base = td; base < total; base += B8 * kDequantThreads) {
-                uint16_t sv[B8];
-                uint8_t zv[B8];
-                int dst[B8];
-#pragma unroll
-                for (int u = 0; u < B8; ++u) {
-                    const int i = base + u * kDequantThreads;
-                    dst[u] = -1;
-                    if (i < total) {
-                        const int j = i / (BM * ng), rem = i - j * BM * ng, r = rem / ng, g = rem - r * ng;
-                        const size_t gi = (size_t)(n0 + r) * gpr + g0 + g;
-                        sv[u] = __ldg(W[j].scales + gi);
-                        zv[u] = (__ldg(W[j].zeros + (gi >> 1)) >> ((gi & 1) * 4)) & 15;
-                        dst[u] = (j * BM + r) * ngs + g;
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < B8; ++u)
-                    if (dst[u] >= 0) {
-                        sc_s[dst[u]] = sv[u];
-                        z_s[dst[u]] = zv[u];
-                    }
-            }
-        }
-        asm volatile("bar.sync 1, %0;" ::"n"(kDequantThreads));
+        const uint16_t* sc_s = reinterpret_cast<const uint16_t*>(smem + args.sc_off);
+        const uint8_t* z_s = smem + args.z_off;
+        (void)ng;
+        mbar_wait(s_full, 0);                    // scales / zeros of the block landed (bulk copies)
+        if (td == 0) k3_stamp(args.diag, NMAT, 1);
         const int swz = nl & 7;
         static_assert(CK == 2, "two dequant groups alternate over the 2 k-tiles of a code stage");
         for (int cj = 0; cj < NCS; ++cj) {
@@ -335,17 +341,18 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
                 if (kt >= AS) mbar_wait(&a_empty[sa], ((kt / AS) - 1) & 1);      // tensor cores done with A[sa]
                 uint8_t* a_tile = smem + S::A_OFF + sa * S::A_STAGE;
                 const uint8_t* c_tile = smem + S::C_OFF + cs * S::C_STAGE;
-                const int g = (((kt0 + kt) * BK + 32 * half) >> gshift) - g0;
+                const int g = ((kt0 + kt) * BK + 32 * half) >> gshift;      // absolute group of the row
 #pragma unroll
-                for (int j = 0; j < NMAT; ++j) {
+                for (int j = 0; j < (args.diag == 2 ? 0 : NMAT); ++j) {
                     // SWIZZLE_64B code tiles: 16-B chunk u of row r sits at u ^ ((r >> 1) & 3),
                     // so the 32 rows a warp reads hit distinct banks
                     const int chunk = (2 * dg + half) ^ ((nl >> 1) & 3);
                     const uint4 c = *reinterpret_cast<const uint4*>(c_tile + j * kCodeTile + nl * (CK * 32) +
                                                                     chunk * 16);
-                    const uint32_t z = z_s[(j * BM + nl) * ngs + g];
+                    const int zi = (j * BM + nl) * gpr + g;                      // nibble index in the block
+                    const uint32_t z = (z_s[zi >> 1] >> ((zi & 1) << 2)) & 15u;
                     const uint32_t zz = (0x4300u | z) * 0x00010001u;
-                    const uint32_t ss = (uint32_t)sc_s[(j * BM + nl) * ngs + g] * 0x00010001u;
+                    const uint32_t ss = (uint32_t)sc_s[(j * BM + nl) * gpr + g] * 0x00010001u;
                     if constexpr (S::A_TMEM) {
                         uint32_t o[16];
                         dequant32_regs(c, zz, ss, o);
@@ -368,15 +375,19 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
         }
 
         // ---------------------------------------------------------- epilogue
-        if (warp < kFirstDequantWarp + 4) {
+        {
+            // all 16 dequant warps: warp w reads TMEM lane quadrant w % 4 and
+            // takes every 4th 16-column chunk of the token tile
             const int q = warp & 3;                   // TMEM lane quadrant of this warp
+            const int part = (warp - kFirstDequantWarp) >> 2;
             const int nrow = n0 + 32 * q + lane;
             mbar_wait(tmem_full, 0);
+            if (threadIdx.x == 32 * kFirstDequantWarp) k3_stamp(args.diag, NMAT, 4);
             tc_fence_after();
             const uint32_t lane_addr = tmem_base + ((uint32_t)(32 * q) << 16);
             const int row0 = args.row_start[e] + m0;
             const int valid = min(args.n_eff, rows - m0);
-            for (int c0 = 0; c0 < args.n_eff; c0 += 16) {
+            for (int c0 = 16 * part; c0 < args.n_eff; c0 += 64) {
                 uint32_t d1[16];
                 tmem_ld16(lane_addr + c0, d1);
                 if constexpr (NMAT == 2) {
@@ -404,6 +415,7 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
     }
     tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) k3_stamp(args.diag, NMAT, 5);
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc<TMEM_COLS>(tmem_base);
@@ -593,6 +605,8 @@ static int grouped_ffn_impl(const void* xperm, const int32_t* row_start, const i
         total_rows = std::max(total_rows, row_start[i] + nrows[i]);
     }
     GemmArgs a1{}, a2{};
+    static const int diag = getenv("DS_K3_TIMELINE") ? 8 : (getenv("DS_K3_DIAG") ? atoi(getenv("DS_K3_DIAG")) : 0);
+    a1.diag = a2.diag = diag;
     // token tile: 256 rows (UMMA N = 256) once an expert has more than 128 rows,
     // so its weights are dequantised once instead of once per 128-row block
     int max_rows = 0;
@@ -738,4 +752,13 @@ extern "C" int ds_w4_linear_gemm(const void* x, int rows, const ds_w4_linear* w,
         DS_LAUNCH_CHECK("ds_w4_linear_gemm: split reduce");
     }
     return DS_OK;
+}
+
+// Diagnostics: per-CTA stamps of the last K3 launches made with DS_K3_TIMELINE=1
+// (nmat = 2: GEMM1, 1: GEMM2; out [n_ctas][8] u64 ns).
+extern "C" int ds_debug_k3_timeline(unsigned long long* out, int nmat, int n_ctas) {
+    DS_CHECK_ARG(out && (nmat == 1 || nmat == 2) && n_ctas > 0 && n_ctas <= 1024, "ds_debug_k3_timeline: bad args");
+    cudaError_t e = cudaMemcpyFromSymbol(out, ds::g_k3_dbg, (size_t)n_ctas * 8 * sizeof(unsigned long long),
+                                         (size_t)(nmat - 1) * 1024 * 8 * sizeof(unsigned long long));
+    return cuda_status(e, "ds_debug_k3_timeline");
 }
