@@ -231,6 +231,11 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
         for (int j = 0; j < NMAT; ++j) tma_prefetch_desc(&args.codes_map[e][j]);
     }
     if (threadIdx.x == 0) k3_stamp(args.diag, NMAT, 0);
+    // GEMM1 lets the dependent launch (GEMM2, programmatic stream
+    // serialization) start at once: its CTAs take the SMs GEMM1 leaves idle
+    // and stage their scales and W2 codes; only their activation (H) loads
+    // wait for GEMM1 (griddepcontrol.wait below)
+    if constexpr (NMAT == 2) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
     tc_fence_before();
     __syncthreads();
@@ -266,6 +271,9 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
     } else if (warp == 1) {
         // ----------------------------------------- activation producer (L2)
         if (lane == 0) {
+            // the activations may be the previous kernel's output (GEMM2 reads
+            // GEMM1's H): wait for it (a no-op without a programmatic dependency)
+            asm volatile("griddepcontrol.wait;" ::: "memory");
             const int row_coord = args.row_start[e] + m0;
             for (int kt = 0; kt < KT; ++kt) {
                 const int s = kt % BS;
@@ -497,9 +505,19 @@ int launch_gemm(const CUtensorMap& map, GemmArgs& a, int E, int max_mblocks, cud
         if (e != cudaSuccess) return cuda_status(e, "w4_gemm: smem attribute");
         attr = true;
     }
-    dim3 grid((a.N / BM) * a.splits, max_mblocks, E);
-    w4_gemm_kernel<NMAT, TN><<<grid, kThreads, a.smem_bytes, st>>>(map, a);
-    DS_LAUNCH_CHECK("w4_gemm launch");
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((a.N / BM) * a.splits, max_mblocks, E);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = a.smem_bytes;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // may start during the previous kernel
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    static const bool pdl = !(getenv("DS_K3_PDL") && getenv("DS_K3_PDL")[0] == '0');   // A/B runs
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaError_t er = cudaLaunchKernelEx(&cfg, w4_gemm_kernel<NMAT, TN>, map, a);
+    if (er != cudaSuccess) return cuda_status(er, "w4_gemm launch");
     return DS_OK;
 }
 
