@@ -94,7 +94,11 @@ struct Smem {
     // accumulators 2 x 160 columns + 3 A stages x 64 columns = all 512
     static constexpr bool A_TMEM = TN <= 160;
     static constexpr int AS = (NMAT == 2 && TN == 256) ? 2 : (TN == 160 ? 3 : 4);
-    static constexpr int BS = TN == 256 ? (NMAT == 2 ? 2 : 3) : 4;   // activation stages
+#ifndef DS_K3_BS
+#define DS_K3_BS 4
+#endif
+    // activation stages: L2-resident tiles, but ~1-2 us of TMA latency each
+    static constexpr int BS = TN == 256 ? (NMAT == 2 ? 2 : 3) : DS_K3_BS;
     static constexpr int A_STAGE = NMAT * kTileBytes;
     static constexpr int B_STAGE = TN * 128;
     static constexpr int C_STAGE = NMAT * kCodeTile;
