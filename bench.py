@@ -754,6 +754,16 @@ def run_sweep(args):
             rows = [r for _, _, gates in eng._batch_sets for r in gates]
             kern = prof.summary(measured_peaks())
             hs = eng.hit_summary()
+            par = None
+            if not args.no_parity:               # oracle checker leg (test infrastructure, untimed)
+                from oracle import check_request, predictor_ref
+                from paper_2509_07379_b200 import predictor as P_
+                with tempfile.TemporaryDirectory() as td:
+                    P_.save_model(net, Path(td) / "net.bin")
+                    ref_net = predictor_ref.load_container(Path(td) / "net.bin")
+                par = check_request.check_request_batch(eng.log, eng.paths_prefill, eng.paths_decode,
+                                                        eng._batch_sets, shape.num_layers, shape.top_k, ref_net,
+                                                        pop.values, aff.values)
             points.append({
                 "batch": B, "prompt": P, "decode_steps": D, "ttft_ms": round(ttft, 2),
                 "decode_ms_per_step": round(dec_ms / D, 3),
@@ -764,6 +774,7 @@ def run_sweep(args):
                 "decode_rows_per_expert": round(B * shape.top_k / max(sum(dec_act) / max(len(dec_act), 1), 1e-9), 3),
                 "predictor": {k: hs[k] for k in ("topk_hit_rate", "at_least_one_rate", "prefetch_hits",
                                                  "prefetch_misses")},
+                "parity": par,
                 "h2d_gb_per_request": round(h2d / 1e9, 3),
                 "peak_device_gb": round(torch.cuda.max_memory_allocated(dev) / 1e9, 3),
                 "kernels": [{k: r[k] for k in ("kernel", "launches", "avg_us", "achieved", "unit", "frac")}

@@ -108,3 +108,26 @@ def test_batch_rows_match_single_sequences(tiny, cuda):
         assert rel < 2e-2, (b, rel)
         same = (bat.paths_prefill[b * Pl:(b + 1) * Pl] == one.paths_prefill).all(axis=-1).mean()
         assert same >= 0.95, (b, same)
+
+
+@pytest.mark.parametrize("B,Pl,D", [(4, 128, 4)])
+def test_batch_8x7b_shapes(cuda, tmp_path, B, Pl, D):
+    """BatchEngine at Mixtral-8x7B shapes (the config-4 sweep's engine): routing
+    teacher forced on every routed row, every sequence's predicted sets and the
+    union cache log vs the oracle — with the K4 R-row GEMV and the tcgen05 GEMM
+    on the real expert shapes."""
+    shape = C.load_shape("mixtral-8x7b")
+    net, pop, aff = _inputs(shape)
+    L = shape.num_layers
+    eng = BatchEngine(shape, "duoserve", batch=B, seed=0, device=cuda, predictor=net, pop=pop, aff=aff,
+                      max_prompt=Pl, max_seq=Pl + D + 4)
+    eng.capture = []
+    ids = torch.randint(0, shape.vocab, (B, Pl), generator=torch.Generator().manual_seed(21))
+    eng.generate(ids, D)
+    r = check_request.check_routing(eng.capture, [eng.W.layers[l]["wg"] for l in range(L)], 2)
+    assert r["mismatches"] == 0 and r["routed_tokens"] == B * Pl * L + B * (D - 1) * L, r
+    c = check_request.check_request_batch(eng.log, eng.paths_prefill, eng.paths_decode, eng._batch_sets, L, 2,
+                                          _ref_net(net, tmp_path), pop.values, aff.values)
+    assert c["set_mismatches"] == 0 and c["log_equal"], c
+    eng.close()
+    eng.store.close()
