@@ -5,7 +5,7 @@
 #   gpurun --timeout 2400 -- bash scripts/gpu_round.sh [steps...]
 set -u
 mkdir -p gpurun_out
-STEPS="${*:-probe tests smoke bench kbench launches ncu}"
+STEPS="${*:-probe tests smoke bench kbench timelines launches ncu}"
 log() { echo "== $(date +%T) $*" | tee -a gpurun_out/round.log; }
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.used --format=csv >> gpurun_out/round.log 2>&1
 for s in $STEPS; do
@@ -16,7 +16,12 @@ for s in $STEPS; do
     bench)  log bench;  timeout 1500 python bench.py --steps 2 --warmup 3 --out gpurun_out/bench.json > gpurun_out/bench.log 2>&1; log "bench rc=$?";;
     bench22) log bench22; timeout 2400 python bench.py --config mixtral-8x22b --steps 1 --warmup 3 --warmup-decode 8 --no-cpu-baseline --out gpurun_out/bench22.json > gpurun_out/bench22.log 2>&1; log "bench22 rc=$?";;
     benchref) log benchref; timeout 600 python bench.py --impl reference --steps 1 --warmup 1 > gpurun_out/bench_ref.log 2>&1; log "benchref rc=$?";;
-    sweep)  log sweep;  timeout 900 python scripts/sweep.py --out gpurun_out/sweep.json > gpurun_out/sweep.log 2>&1; log "sweep rc=$?";;
+    sweep)  log sweep;  timeout 2400 python bench.py --sweep --sweep-decode 8 --out gpurun_out/sweep.json > gpurun_out/sweep.log 2>&1; log "sweep rc=$?";;
+    timelines) log timelines
+      timeout 300 python scripts/k4v6_timeline.py > gpurun_out/k4v6_timeline.json 2>&1
+      timeout 300 python scripts/k3_timeline.py 151 > gpurun_out/k3_timeline.json 2>&1
+      timeout 300 python scripts/k4_ce2.py --out gpurun_out/k4_ce2.json > gpurun_out/k4_ce2.log 2>&1
+      log "timelines done";;
     benchpa) log benchpa; timeout 1500 python bench.py --policy prefetchall --steps 1 --warmup 3 --decode 32 --warmup-decode 4 --no-cpu-baseline --out gpurun_out/bench_pa.json > gpurun_out/bench_pa.log 2>&1; log "benchpa rc=$?";;
     benchod) log benchod; timeout 1500 python bench.py --policy ondemand --steps 1 --warmup 3 --decode 32 --warmup-decode 4 --no-cpu-baseline --out gpurun_out/bench_od.json > gpurun_out/bench_od.log 2>&1; log "benchod rc=$?";;
     benchor) log benchor; timeout 1500 python bench.py --policy oracle --steps 1 --warmup 3 --decode 32 --warmup-decode 4 --no-cpu-baseline --out gpurun_out/bench_or.json > gpurun_out/bench_or.log 2>&1; log "benchor rc=$?";;
@@ -31,7 +36,7 @@ for s in $STEPS; do
       python scripts/summarize_launches.py gpurun_out/launches.csv > gpurun_out/launches_summary.md 2>&1;;
     ncu)
       log ncu
-      DS_LAUNCH_GATE=0 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'staged_gemv|swiglu_gemv|down_gemv' -s 4 -c 4 \
+      DS_LAUNCH_GATE=0 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'expert_fused_v6|staged_gemv|swiglu_gemv|down_gemv' -s 4 -c 4 \
         -o gpurun_out/k4 -f python scripts/kbench.py --only k4 --iters 3 > gpurun_out/ncu_k4.log 2>&1
       log "ncu k4 rc=$?"
       DS_LAUNCH_GATE=0 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'w4_gemm' -s 4 -c 2 \

@@ -126,3 +126,15 @@ def test_stub_predictors():
     assert P.OraclePredictor().predict(t, 1) == (2, 3)
     assert P.ComplementPredictor(8).predict(t, 1) == (0, 1)
     assert P.ComplementPredictor(8).predict(t, 2) == (0, 1)
+
+
+def test_bench_arms_share_the_workload_config():
+    """bench.py: the reference arm's `config` is the same dict as ours (the
+    driver compares the two lines' configs)."""
+    import argparse
+    import bench
+    from paper_2509_07379_b200.config import load_shape
+    a = argparse.Namespace(prefill=512, decode=128)
+    c = bench.workload_config(load_shape("mixtral-8x7b"), a)
+    assert c == bench.workload_config(load_shape("mixtral-8x7b"), a, 1)
+    assert c["seq_len"] == 640 and c["model"] == "mixtral-8x7b" and "l2" in c
