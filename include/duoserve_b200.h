@@ -179,6 +179,24 @@ int ds_w4_down_gemv(const void *h, int R, const ds_w4_expert *e, int d, int ff, 
 int ds_w4_expert_gemv(const void *x, int R, const ds_w4_expert *e, int d, int ff, int G, void *h,
                       const float *route_w, int route_stride, float *acc, void *ev_start, void *ev_end,
                       void *stream);
+/* The same expert FFN as ONE launch of a cached, device-uploaded CUDA graph:
+ * [stream waits wait_event (the slot's ready event; may be NULL)] ->
+ * ev_start -> K4 -> ev_end.  While the copy engine streams experts, commands
+ * submitted from the host reach the GPU ~25-30 us late (the front end fetches
+ * them over the busy host link); inside an uploaded graph the wait, the span
+ * events and the launches run from device memory.  Graphs are keyed by every
+ * argument except the three events (swapped per launch); R <= 16.
+ * Replaces the per-expert FFN call of the reference's decode loop
+ * ("vLLM AWQ operators"; SPEC.md:383-391 decode compute).     */
+int ds_w4_expert_gemv_graph(const void *x, int R, const ds_w4_expert *e, int d, int ff, int G, void *h,
+                            const float *route_w, int route_stride, float *acc, void *wait_event,
+                            void *ev_start, void *ev_end, void *stream);
+/* Destroy every cached K4 graph (their static buffers are being freed).    */
+int ds_w4_graph_cache_clear(void);
+/* Device-clock (%globaltimer) totals of every fused K4 launch so far: the sum
+ * of first-CTA-entry -> last-CTA-exit in ns and the launch count (synchronous
+ * read; the profiler's in-loop kernel duration beside its CUDA-event spans). */
+int ds_k4_device_span(unsigned long long *ns, unsigned long long *n);
 /* ------------------------------------------------------------------------
  * Plain W4 linears: the non-MoE projections (attention q|k|v and o) kept
  * resident in HBM in the same W4 format, so the non-MoE weights fit the

@@ -27,6 +27,8 @@
 #include <cstdlib>
 #include <map>
 #include <mutex>
+#include <cstring>
+#include <vector>
 
 namespace ds {
 namespace {
@@ -1209,6 +1211,14 @@ __device__ unsigned g_k4f_bar[k4s::kTicketSlots];
 // launch — entry, phase A consumed, grid barrier passed, h staged, exit
 __device__ unsigned long long g_k4f_dbg[1024 * 8];
 __device__ unsigned g_k4f_exit[k4s::kTicketSlots];
+// always-on device-clock span of every v6 launch: first CTA entry -> last CTA
+// exit on %globaltimer (entries kept as ~t so a zero-initialised atomicMax
+// finds the earliest), accumulated over launches.  CUDA-event spans on the
+// launching stream also contain the front end's event-timestamp cost, which
+// grows from ~7 to ~29 us while the copy engine streams host memory
+// (scripts/launchprobe.cu); this is the kernel's own duration beside them.
+__device__ unsigned long long g_k4f_first[k4s::kTicketSlots];
+__device__ unsigned long long g_k4f_span_ns, g_k4f_span_n;
 
 template <int KA, int KB, int RBA, int RBB>
 __global__ void __launch_bounds__(k4f::kThreads, 1) expert_fused_v6_kernel(
@@ -1224,6 +1234,11 @@ __global__ void __launch_bounds__(k4f::kThreads, 1) expert_fused_v6_kernel(
         }
     };
     stamp(0);
+    if (threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        atomicMax(g_k4f_first + slot_id, ~t);
+    }
     constexpr int GPRA = Gm::GPRA, GPRB = Gm::GPRB;
     constexpr int TA = KB / Gm::RBA;                 // phase-A tiles: rows of W1 / W3 (N = ff = KB)
     constexpr int TB = KA / Gm::RBB;                 // phase-B tiles: rows of W2 (N = d = KA)
@@ -1524,6 +1539,11 @@ __global__ void __launch_bounds__(k4f::kThreads, 1) expert_fused_v6_kernel(
     if (threadIdx.x == 0) {
         __threadfence();
         if (atomicAdd(g_k4f_exit + slot_id, 1u) == gridDim.x - 1) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            const unsigned long long first = ~atomicExch(g_k4f_first + slot_id, 0ull);
+            atomicAdd(&g_k4f_span_ns, t - first);
+            atomicAdd(&g_k4f_span_n, 1ull);
             atomicExch(g_k4f_bar + slot_id, 0u);
             atomicExch(g_k4f_exit + slot_id, 0u);
         }
@@ -1853,6 +1873,181 @@ extern "C" int ds_w4_expert_gemv(const void* x, int R, const ds_w4_expert* e, in
     return rc;
 }
 
+// ---------------------------------------------------------------------------
+// K4 through a CUDA graph.  While the copy engine streams an expert over the
+// host link (97 % of decode), every command the host submits reaches the GPU
+// ~25-30 us late: the front end fetches the pushbuffer from host memory behind
+// the copy engine's queued PCIe reads (profiles/r2/k4_ce_timeline.json: the v6
+// kernel itself runs 28.0 -> 28.7 us beside the copy, its event span 47 ->
+// 60 us).  An uploaded graph lives in device memory, so one graph launch
+// carries [wait for the slot's ready event] -> ev_start -> K4 -> ev_end with
+// no further host fetch between the data landing and the kernel starting.
+// Graphs are cached per argument set (static decode buffers: 4-8 slots x k
+// routing columns + pinned experts); the events are swapped per launch.
+namespace {
+struct K4GraphKey {
+    const void* x; const void* h; const float* rw; const float* acc; ds_w4_expert e;
+    int R, d, ff, G, rs; bool wait, evs; int dev;
+    bool operator<(const K4GraphKey& o) const { return std::memcmp(this, &o, sizeof(*this)) < 0; }
+};
+struct K4Graph {
+    cudaGraph_t graph = nullptr;      // kept: its node handles address the exec's nodes
+    cudaGraphExec_t exec = nullptr;
+    cudaGraphNode_t wait = nullptr, start = nullptr, end = nullptr;
+    // library-owned placeholder events: the nodes point at these between
+    // launches, never at a caller's event that may since have been destroyed
+    cudaEvent_t own[3] = {nullptr, nullptr, nullptr};
+};
+
+void k4g_destroy(K4Graph& g) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (g.graph) cudaGraphDestroy(g.graph);
+    for (auto& e : g.own)
+        if (e) cudaEventDestroy(e);
+    g = K4Graph();
+}
+std::mutex g_k4g_mu;
+std::map<K4GraphKey, K4Graph> g_k4g;
+constexpr size_t kK4GraphCap = 1024;
+
+void k4g_clear_locked() {
+    for (auto& kv : g_k4g) k4g_destroy(kv.second);
+    g_k4g.clear();
+}
+
+int k4g_capture(const K4GraphKey& k, cudaEvent_t wait_ev, cudaEvent_t e0, cudaEvent_t e1, cudaGraph_t* gout);
+
+int k4g_build(const K4GraphKey& k, K4Graph* out) {
+    for (auto& e : out->own)
+        if (cudaEventCreate(&e) != cudaSuccess) {
+            k4g_destroy(*out);
+            return fail(DS_ERR_STATE, "ds_w4_expert_gemv_graph: placeholder events");
+        }
+    cudaGraph_t g = nullptr;
+    int rc = k4g_capture(k, out->own[0], out->own[1], out->own[2], &g);
+    if (rc) {
+        k4g_destroy(*out);
+        return rc;
+    }
+    cudaError_t er;
+
+    size_t n = 0;
+    cudaGraphGetNodes(g, nullptr, &n);
+    std::vector<cudaGraphNode_t> nodes(n);
+    cudaGraphGetNodes(g, nodes.data(), &n);
+    for (auto nd : nodes) {
+        cudaGraphNodeType t;
+        cudaGraphNodeGetType(nd, &t);
+        size_t n_dep = 0, n_out = 0;
+        cudaGraphNodeGetDependencies(nd, nullptr, &n_dep);
+        cudaGraphNodeGetDependentNodes(nd, nullptr, &n_out);
+        if (getenv("DS_K4G_DEBUG"))
+            fprintf(stderr, "[k4 graph] node %p type %d deps %zu dependents %zu\n", (void*)nd, (int)t, n_dep, n_out);
+        if (t == cudaGraphNodeTypeWaitEvent) {
+            out->wait = nd;
+        } else if (t == cudaGraphNodeTypeEventRecord) {
+            // the span's end is the record node nothing depends on
+            (n_out == 0 ? out->end : out->start) = nd;
+        }
+    }
+    out->graph = g;
+    er = cudaGraphInstantiate(&out->exec, g, 0);
+    if (er != cudaSuccess) {
+        k4g_destroy(*out);
+        return cuda_status(er, "ds_w4_expert_gemv_graph: instantiate");
+    }
+    if ((k.wait && !out->wait) || (k.evs && (!out->start || !out->end))) {
+        k4g_destroy(*out);
+        return fail(DS_ERR_STATE, "ds_w4_expert_gemv_graph: captured graph lacks its event nodes");
+    }
+    return DS_OK;
+}
+int k4g_capture(const K4GraphKey& k, cudaEvent_t wait_ev, cudaEvent_t e0, cudaEvent_t e1, cudaGraph_t* gout) {
+    static thread_local cudaStream_t caps[64] = {};        // private capture stream per device (never runs work)
+    cudaStream_t& cap = caps[k.dev & 63];
+    if (!cap && cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) != cudaSuccess)
+        return fail(DS_ERR_STATE, "ds_w4_expert_gemv_graph: capture stream");
+    // relaxed: the link thread keeps issuing copies while this thread captures
+    cudaError_t er = cudaStreamBeginCapture(cap, cudaStreamCaptureModeRelaxed);
+    if (er != cudaSuccess) return cuda_status(er, "ds_w4_expert_gemv_graph: begin capture");
+    int rc = DS_OK;
+    if (k.wait) er = cudaStreamWaitEvent(cap, wait_ev, cudaEventWaitExternal);
+    if (er == cudaSuccess && k.evs) er = cudaEventRecordWithFlags(e0, cap, cudaEventRecordExternal);
+    if (er != cudaSuccess) rc = cuda_status(er, "ds_w4_expert_gemv_graph: capture events");
+    if (!rc) rc = expert_v6(k.x, k.R, &k.e, k.d, k.ff, k.G, const_cast<void*>(k.h), k.rw,
+                            const_cast<float*>(k.acc), cap);
+    if (rc == 1) {
+        rc = ds_w4_swiglu_gemv(k.x, k.R, &k.e, k.d, k.ff, k.G, const_cast<void*>(k.h), cap);
+        if (!rc) rc = ds_w4_down_gemv(k.h, k.R, &k.e, k.d, k.ff, k.G, k.rw, k.rs, const_cast<float*>(k.acc), cap);
+    }
+    if (!rc && k.evs) {
+        er = cudaEventRecordWithFlags(e1, cap, cudaEventRecordExternal);
+        if (er != cudaSuccess) rc = cuda_status(er, "ds_w4_expert_gemv_graph: capture events");
+    }
+    cudaGraph_t g = nullptr;
+    er = cudaStreamEndCapture(cap, &g);
+    if (!rc && er != cudaSuccess) rc = cuda_status(er, "ds_w4_expert_gemv_graph: end capture");
+    if (rc) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+    }
+    *gout = g;
+    return DS_OK;
+}
+}  // namespace
+
+extern "C" int ds_w4_expert_gemv_graph(const void* x, int R, const ds_w4_expert* e, int d, int ff, int G,
+                                       void* h, const float* route_w, int route_stride, float* acc,
+                                       void* wait_event, void* ev_start, void* ev_end, void* stream) {
+    DS_CHECK_ARG(x && e && h && route_w && acc && R >= 1 && R <= 16, "ds_w4_expert_gemv_graph: bad arguments");
+    DS_CHECK_ARG((ev_start == nullptr) == (ev_end == nullptr), "ds_w4_expert_gemv_graph: events come in pairs");
+    cudaStream_t st = as_stream(stream);
+    K4GraphKey k;
+    std::memset(&k, 0, sizeof(k));                           // padding bytes take part in the key
+    k.x = x; k.h = h; k.rw = route_w; k.acc = acc; k.e = *e;
+    k.R = R; k.d = d; k.ff = ff; k.G = G; k.rs = route_stride;
+    k.wait = wait_event != nullptr; k.evs = ev_start != nullptr;
+    cudaGetDevice(&k.dev);
+    auto w_ev = reinterpret_cast<cudaEvent_t>(wait_event);
+    auto e0 = reinterpret_cast<cudaEvent_t>(ev_start), e1 = reinterpret_cast<cudaEvent_t>(ev_end);
+    std::lock_guard<std::mutex> lk(g_k4g_mu);
+    auto it = g_k4g.find(k);
+    if (it == g_k4g.end()) {
+        if (g_k4g.size() >= kK4GraphCap) k4g_clear_locked();
+        K4Graph kg;
+        int rc = k4g_build(k, &kg);
+        if (rc) return rc;
+        cudaError_t er = cudaGraphUpload(kg.exec, st);       // device-resident before its first launch
+        if (er != cudaSuccess) {
+            k4g_destroy(kg);
+            return cuda_status(er, "ds_w4_expert_gemv_graph: upload");
+        }
+        it = g_k4g.emplace(k, kg).first;
+    }
+    K4Graph& kg = it->second;
+    // point the nodes at this call's events, launch, point them back at the
+    // placeholders (exec updates never affect a launch already submitted)
+    auto set = [&](cudaEvent_t w, cudaEvent_t a, cudaEvent_t b) -> cudaError_t {
+        cudaError_t er = cudaSuccess;
+        if (k.wait) er = cudaGraphExecEventWaitNodeSetEvent(kg.exec, kg.wait, w);
+        if (er == cudaSuccess && k.evs) er = cudaGraphExecEventRecordNodeSetEvent(kg.exec, kg.start, a);
+        if (er == cudaSuccess && k.evs) er = cudaGraphExecEventRecordNodeSetEvent(kg.exec, kg.end, b);
+        return er;
+    };
+    cudaError_t er = set(w_ev, e0, e1);
+    if (er != cudaSuccess) return cuda_status(er, "ds_w4_expert_gemv_graph: set events");
+    er = cudaGraphLaunch(kg.exec, st);
+    cudaError_t er2 = set(kg.own[0], kg.own[1], kg.own[2]);
+    if (er != cudaSuccess) return cuda_status(er, "ds_w4_expert_gemv_graph: launch");
+    return er2 == cudaSuccess ? DS_OK : cuda_status(er2, "ds_w4_expert_gemv_graph: reset events");
+}
+
+extern "C" int ds_w4_graph_cache_clear(void) {
+    std::lock_guard<std::mutex> lk(g_k4g_mu);
+    k4g_clear_locked();
+    return DS_OK;
+}
+
 extern "C" int ds_combine_finalize(float* acc, const void* resid, int R, int d, void* out,
                                    void* stream) {
     DS_CHECK_ARG(R >= 0 && d > 0, "ds_combine_finalize: bad shape");
@@ -1865,6 +2060,15 @@ extern "C" int ds_combine_finalize(float* acc, const void* resid, int R, int d, 
                                                          (__nv_bfloat16*)out);
     DS_LAUNCH_CHECK("ds_combine_finalize");
     return DS_OK;
+}
+
+// Device-clock totals of every fused (v6) K4 launch since the library loaded:
+// sum of (last CTA exit - first CTA entry) in ns and the launch count.
+extern "C" int ds_k4_device_span(unsigned long long* ns, unsigned long long* n) {
+    DS_CHECK_ARG(ns && n, "ds_k4_device_span: NULL pointer");
+    cudaError_t e = cudaMemcpyFromSymbol(ns, g_k4f_span_ns, sizeof(*ns));
+    if (e == cudaSuccess) e = cudaMemcpyFromSymbol(n, g_k4f_span_n, sizeof(*n));
+    return cuda_status(e, "ds_k4_device_span");
 }
 
 // Diagnostics: the per-CTA stamps of the last v6 launch run with DS_K4_V6_TIMELINE=1

@@ -35,6 +35,7 @@ filling while the current one computes.
 
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass
 
@@ -218,6 +219,11 @@ class ExpertCache:
         torch.cuda.current_stream(self.device).wait_event(self.ready[slot])
         return self._structs[slot]
 
+    def struct(self, slot: int) -> "object":
+        """The slot's expert struct without a stream wait (the caller passes
+        ready[slot] to a graph launch that waits on the device)."""
+        return self._structs[slot]
+
     def release(self, slot: int) -> None:
         self.free[slot].record(torch.cuda.current_stream(self.device))
         self.used[slot] = True
@@ -378,13 +384,14 @@ class MLPDriver:
     def launch(self, hist: torch.Tensor, after: torch.cuda.Event, target_layer: int) -> None:
         with torch.cuda.stream(self.stream):
             self.stream.wait_event(after)
-            if self.prof is not None:
+            timed = self.prof is not None
+            if timed:
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(self.stream)
             self.dev.predict_state(hist, self.targets[target_layer], self.stats.pop, self.stats.aff, self.L,
                                    self.M, self.k, self.mode, self.k, out=self.out, probs=self.probs,
                                    stream=self.stream)
-            if self.prof is not None:
+            if timed:
                 e1.record(self.stream)
                 self.prof.add("K5 predictor (fused f64 MLP)", e0, e1, self.dev.nbytes)
             self.host_out.copy_(self.out, non_blocking=True)
@@ -463,6 +470,8 @@ class Engine:
                               link_depth if cancel_mispredicted else 2, cancel_mispredicted,
                               spec_chunk_bytes=int(spec_chunk_mb * 2**20))
         self.max_seq, self.max_prefill = int(max_seq), int(max_prefill)
+        # K4 as one device-resident graph launch per expert (A/B: DS_K4_GRAPH=0)
+        self.k4_graphs = os.environ.get("DS_K4_GRAPH", "1") != "0"
         self.kv = self._make_kv(max_seq)
         self.cos, self.sin = rope_tables(sh, max_seq, self.device)
         self.driver = None
@@ -586,6 +595,7 @@ class Engine:
         torch.cuda.synchronize(self.device)
         self.link.close()
         self.g_graphs = None
+        ops.w4_graph_cache_clear()                      # K4 graphs capture this engine's buffers
         for name in ("p_xperm", "p_h", "p_y", "p_ws", "p_part", "p_paths", "_pinned_buf"):
             setattr(self, name, None)
         self.pinned = {}
@@ -928,7 +938,8 @@ class Engine:
             self.log.append({"phase": "decode", "token": self.t_decode, "layer": l, "fetch": list(self.owned),
                              "kind": "prefetchall"})
             for e in mine:
-                self._decode_ffn(a, self.cache.acquire(self._pa_slot(self._pa_v, e)), E.index(e))
+                sl = self._pa_slot(self._pa_v, e)
+                self._decode_ffn(a, self.cache.struct(sl), E.index(e), wait=self.cache.ready[sl])
             self._pa_done()
             out = self._decode_combine(h, out)
             self._record_moe("decode", l, h, a, out, self.idx_host, self.w1)
@@ -967,7 +978,7 @@ class Engine:
         for e in [x for x in mine if x not in miss] + miss:
             j = E.index(e)
             link.flush(trs[e])
-            self._decode_ffn(a, self.cache.acquire(slot_of[e]), j)
+            self._decode_ffn(a, self.cache.struct(slot_of[e]), j, wait=self.cache.ready[slot_of[e]])
             self.cache.release(slot_of[e])
         out = self._decode_combine(h, out)
         self._record_moe("decode", l, h, a, out, self.idx_host, self.w1)
@@ -984,14 +995,27 @@ class Engine:
             self._pred_next = (Pn, order, pending)
         return out, E
 
-    def _decode_ffn(self, a, st, j: int) -> None:
-        """K4: acc += w_j * W2 (silu(a W1) * (a W3)) for the expert in slot struct st."""
-        if self.prof:
+    def _decode_ffn(self, a, st, j: int, wait=None) -> None:
+        """K4: acc += w_j * W2 (silu(a W1) * (a W3)) for the expert in slot struct st,
+        once `wait` (the slot's ready event; None for a pinned expert) fired.
+
+        Default: one launch of a cached device-resident graph [wait -> span
+        events -> K4] (ops.expert_gemv_graph): while the copy engine streams
+        the next expert, host-submitted commands reach the GPU ~25-30 us late,
+        graph-internal ones do not (profiles/r2/k4_ce_timeline.json)."""
+        ev0 = ev1 = None
+        timed = self.prof is not None
+        if timed:
             ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            ops.expert_gemv(a, st, self.d, self.ff, self.G, self.h_buf, self.w1[0, j:], 1, self.acc, ev0, ev1)
-            self.prof.add("K4 w4_swiglu_gemv+down_gemv", ev0, ev1, self.store.blob_bytes)
+        if self.k4_graphs:
+            ops.expert_gemv_graph(a, st, self.d, self.ff, self.G, self.h_buf, self.w1[0, j:], 1, self.acc,
+                                  wait, ev0, ev1)
         else:
-            ops.expert_gemv(a, st, self.d, self.ff, self.G, self.h_buf, self.w1[0, j:], 1, self.acc)
+            if wait is not None:
+                torch.cuda.current_stream(self.device).wait_event(wait)
+            ops.expert_gemv(a, st, self.d, self.ff, self.G, self.h_buf, self.w1[0, j:], 1, self.acc, ev0, ev1)
+        if timed:
+            self.prof.add("K4 w4_swiglu_gemv+down_gemv", ev0, ev1, self.store.blob_bytes)
 
     def _decode_combine(self, h, out):
         if out is None:
@@ -1481,7 +1505,10 @@ class KernelProfiler:
     def summary(self, peaks: dict) -> dict:
         torch.cuda.synchronize()
         hbm = float(peaks.get("hbm_gbs", 6650.0))
-        tf = float(peaks.get("bf16_tflops", 1590.0))
+        # a K3 launch is timed inside a seconds-long serving step: its roofline
+        # is the SUSTAINED bf16 figure when the driver measured one
+        tf = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1590.0)))
+        tf_kind = "sustained" if "bf16_tflops_sustained" in peaks else "burst"
         out = []
         for name, sp in self.spans.items():
             t = sum(a.elapsed_time(b) for a, b, _, _ in sp) / 1e3
@@ -1490,7 +1517,7 @@ class KernelProfiler:
             if fl > 0:
                 ach = fl / t / 1e12
                 out.append({"kernel": name, "bound": "tensor", "achieved": round(ach, 1), "peak": tf,
-                            "unit": "TFLOP/s", "frac": round(ach / tf, 4), "traffic": None,
+                            "peak_kind": tf_kind, "unit": "TFLOP/s", "frac": round(ach / tf, 4), "traffic": None,
                             "launches": len(sp), "avg_us": round(1e6 * t / len(sp), 2),
                             "total_ms": round(1e3 * t, 2), "bytes_per_launch": nb / len(sp),
                             "flops_per_launch": fl / len(sp)})

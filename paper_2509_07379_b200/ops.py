@@ -132,6 +132,37 @@ def expert_gemv(x: torch.Tensor, e: _lib.W4Expert, d: int, ff: int, G: int, h: t
     _count("ds_w4_down_gemv", n)
 
 
+def expert_gemv_graph(x: torch.Tensor, e: _lib.W4Expert, d: int, ff: int, G: int, h: torch.Tensor,
+                      route_w: torch.Tensor, route_stride: int, acc: torch.Tensor, wait_event=None, ev_start=None,
+                      ev_end=None) -> None:
+    """K4 for one expert as ONE launch of a cached device-resident CUDA graph:
+    [wait for wait_event] -> ev_start -> K4 -> ev_end (csrc/w4.cu,
+    ds_w4_expert_gemv_graph): no host-submitted command sits between the
+    slot's data landing and the kernel starting."""
+    evs = _native_events(ev_start, ev_end)
+    w = None
+    if wait_event is not None:
+        if not wait_event.cuda_event:
+            raise _lib.DeviceError("expert_gemv_graph: wait event was never recorded")
+        w = C.c_void_p(wait_event.cuda_event)
+    _lib.call("ds_w4_expert_gemv_graph", ptr(x), x.shape[0], C.byref(e), d, ff, G, ptr(h), ptr(route_w),
+              route_stride, ptr(acc), w, evs[0], evs[1], stream_ptr())
+    n = _gemv_passes(x.shape[0], G)
+    _count("ds_w4_swiglu_gemv", n)
+    _count("ds_w4_down_gemv", n)
+
+
+def k4_device_span() -> tuple:
+    """(ns, launches): device-clock totals of every fused K4 launch so far."""
+    ns, n = C.c_ulonglong(0), C.c_ulonglong(0)
+    _lib.call("ds_k4_device_span", C.byref(ns), C.byref(n))
+    return ns.value, n.value
+
+
+def w4_graph_cache_clear() -> None:
+    _lib.call("ds_w4_graph_cache_clear")
+
+
 def combine_finalize(acc: torch.Tensor, resid: torch.Tensor, out: torch.Tensor) -> None:
     _lib.call("ds_combine_finalize", ptr(acc), ptr(resid), resid.shape[0], resid.shape[1], ptr(out), stream_ptr())
     _count("ds_combine_finalize")

@@ -346,3 +346,55 @@ def test_grouped_ffn_segments_one_launch(cuda):
         assert rel < 1e-4, (i, rel)
     out = ~inside.to(cuda)
     assert bool((y[out] == -3.0).all()) and bool((h[out] == 7.0).all())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d,ff", [(4096, 14336), (6144, 16384), (256, 896)])
+def test_expert_gemv_graph_matches_eager(cuda, d, ff):
+    """ds_w4_expert_gemv_graph (one launch of a cached device-resident graph:
+    wait on the slot's ready event -> span events -> K4) gives the eager
+    call's h and output bit for bit, on the first (capture) and on repeated
+    (cached, events swapped) launches, after the waited-on copy landed; the
+    device-clock K4 counter advances for the fused 8x7B launch."""
+    import torch
+    from paper_2509_07379_b200 import ops
+    G = 128
+    offs, total = _layout(d, ff, G)
+    src = torch.zeros(total, dtype=torch.uint8, device=cuda)
+    _lib.call("ds_w4_generate", 13, 1, 3, d, ff, G, _lib.ptr(src), _lib.stream_ptr())
+    host = src.cpu().pin_memory()
+    slot = torch.zeros_like(src)
+    e = _expert_struct(slot, offs)
+    x = _rand_bf16((1, d), 1.0, torch.Generator().manual_seed(5)).to(cuda)
+    rw = torch.tensor([0.5], device=cuda)
+    h_ref = torch.empty((1, ff), dtype=torch.bfloat16, device=cuda)
+    a_ref = torch.zeros((1, d), device=cuda)
+    slot.copy_(src)
+    ops.expert_gemv(x, e, d, ff, G, h_ref, rw, 1, a_ref)
+    torch.cuda.synchronize()
+    cs = torch.cuda.Stream()
+    h = torch.empty_like(h_ref)
+    a = torch.zeros_like(a_ref)
+    n0 = ops.k4_device_span()[1]
+    for it in range(3):
+        slot.zero_()
+        a.zero_()
+        torch.cuda.synchronize()
+        ready = torch.cuda.Event()
+        with torch.cuda.stream(cs):
+            slot.copy_(host, non_blocking=True)        # the expert lands only on the copy stream
+            ready.record(cs)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ops.expert_gemv_graph(x, e, d, ff, G, h, rw, 1, a, ready, ev0, ev1)
+        torch.cuda.synchronize()
+        assert torch.equal(h, h_ref), it
+        assert torch.equal(a, a_ref), it
+        assert ev0.elapsed_time(ev1) > 0
+    # no wait event, no span events (a pinned expert outside the profiler's sample)
+    a.zero_()
+    ops.expert_gemv_graph(x, e, d, ff, G, h, rw, 1, a)
+    torch.cuda.synchronize()
+    assert torch.equal(a, a_ref)
+    if (d, ff) == (4096, 14336):
+        assert ops.k4_device_span()[1] >= n0 + 4
+    ops.w4_graph_cache_clear()
