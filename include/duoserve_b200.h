@@ -198,6 +198,22 @@ int ds_w4_graph_cache_clear(void);
  * read; the profiler's in-loop kernel duration beside its CUDA-event spans). */
 int ds_k4_device_span(unsigned long long *ns, unsigned long long *n);
 /* ------------------------------------------------------------------------
+ * Decode front of one token (the non-MoE steps between two MoE layers; no
+ * reference counterpart — the reference has no forward pass — but they sit
+ * in the decode window before sync point 1).  bf16 in / out,
+ * f32 math.
+ * -------------------------------------------------------------------- */
+/* out[R, d] = bf16( (f32(x) * rsqrt(mean(x^2) + eps)) * f32(gamma) )        */
+int ds_rmsnorm(const void *x, int R, int d, const void *gamma, float eps, void *out, void *stream);
+/* h1 = bf16( f32(h) + y ) (y f32, the o projection); a = rmsnorm(h1, gamma) */
+int ds_residual_rmsnorm(const void *h, const float *y, int R, int d, const void *gamma, float eps, void *h1,
+                        void *a, void *stream);
+/* One token's f32 q|k|v row y[(nh + 2 nkv) * hd] -> bf16 -> RoPE(q, k) with
+ * the cos / sin tables [max_seq, hd] (f32) at the device-resident position
+ * *pos; q[nh, hd] out; k, v written into the layer's cache [nkv, max_seq, hd]. */
+int ds_rope_kv_decode(const float *y, int nh, int nkv, int hd, const float *cos_t, const float *sin_t,
+                      const long long *pos, int max_seq, void *q, void *k_cache, void *v_cache, void *stream);
+/* ------------------------------------------------------------------------
  * Plain W4 linears: the non-MoE projections (attention q|k|v and o) kept
  * resident in HBM in the same W4 format, so the non-MoE weights fit the
  * paper's W4 model budget ("2.15 GB"; SPEC.md:392-398 peak

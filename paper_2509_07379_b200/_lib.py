@@ -82,6 +82,9 @@ _SIGS = {
     "ds_w4_expert_gemv": (_I, [_P, _I, C.POINTER(W4Expert), _I, _I, _I, _P, _P, _I, _P, _P, _P, _P]),
     "ds_w4_expert_gemv_graph": (_I, [_P, _I, C.POINTER(W4Expert), _I, _I, _I, _P, _P, _I, _P, _P, _P, _P, _P]),
     "ds_w4_graph_cache_clear": (_I, []),
+    "ds_rmsnorm": (_I, [_P, _I, _I, _P, C.c_float, _P, _P]),
+    "ds_residual_rmsnorm": (_I, [_P, _P, _I, _I, _P, C.c_float, _P, _P, _P]),
+    "ds_rope_kv_decode": (_I, [_P, _I, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P]),
     "ds_k4_device_span": (_I, [C.POINTER(C.c_ulonglong), C.POINTER(C.c_ulonglong)]),
     "ds_combine_finalize": (_I, [_P, _P, _I, _I, _P, _P]),
     "ds_w4_grouped_ffn_workspace": (_SZ, [_I, _I, _I]),

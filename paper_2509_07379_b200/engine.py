@@ -45,7 +45,8 @@ import torch
 from . import ops
 from .config import ModelShape, SchedulerPolicy, model_config_for_shape, slot_count
 from .model import (DenseWeights, KVCache, KVCacheBatch, attention_block, attention_block_batch,
-                    attention_decode_static, attention_decode_static_batch, init_dense_weights, logits_last,
+                    attention_decode_static, attention_decode_static_batch, decode_front_fused, init_dense_weights,
+                    logits_last,
                     rms_norm, rope_tables)
 from .ep import EPConfig, owned_experts, owner_mask
 from .predictor import ExpertMLP, StatsOnDevice, _mode_code
@@ -267,6 +268,21 @@ class LinkQueue:
         for ev in cache.ready + cache.free:
             ev.record(s)
         s.synchronize()
+        # raw handles resolved once: submit/promote/cancel sit between the gate
+        # result and the miss transfer (the decode reaction window), so they
+        # avoid per-call tensor indexing and name lookups
+        self._slot_ptr = [C.c_void_p(t.data_ptr()) for t in cache.slots]
+        self._ready_ev = [C.c_void_p(e.cuda_event) for e in cache.ready]
+        self._free_ev = [C.c_void_p(e.cuda_event) for e in cache.free]
+        st = cache.store.data
+        self._store_base, self._store_s0, self._store_s1 = st.data_ptr(), st.stride(0), st.stride(1)
+        lib = _lib.load()
+        self._f_submit, self._f_submit_chunked = lib.ds_link_submit, lib.ds_link_submit_chunked
+        self._f_promote, self._f_cancel = lib.ds_link_promote, lib.ds_link_cancel
+
+    def _check(self, rc: int, name: str) -> None:
+        if rc != 0:
+            raise self.lib.DeviceError(name, rc, self.lib.load().ds_last_error().decode(errors="replace"))
 
     def close(self) -> None:
         """Stop the native scheduler thread (idempotent)."""
@@ -288,27 +304,27 @@ class LinkQueue:
         c = self.cache
         C = self.C
         t = C.c_uint64()
-        wait = C.c_void_p(c.free[slot].cuda_event) if c.used[slot] else None
-        args = (self.handle, C.c_void_p(c.slots[slot].data_ptr()), C.c_void_p(c.store.blob(layer, expert).data_ptr()),
-                c.store.blob_bytes)
+        wait = self._free_ev[slot] if c.used[slot] else None
+        src = self._store_base + layer * self._store_s0 + c.store.local[expert] * self._store_s1
+        args = (self.handle, self._slot_ptr[slot], C.c_void_p(src), c.store.blob_bytes)
         if speculative and self.cancel_enabled and self.spec_chunk < self.chunk:
-            self.lib.call("ds_link_submit_chunked", *args, self.spec_chunk, wait, C.c_void_p(c.ready[slot].cuda_event),
-                          C.byref(t))
+            self._check(self._f_submit_chunked(*args, self.spec_chunk, wait, self._ready_ev[slot], C.byref(t)),
+                        "ds_link_submit_chunked")
         else:
-            self.lib.call("ds_link_submit", *args, wait, C.c_void_p(c.ready[slot].cuda_event), C.byref(t))
+            self._check(self._f_submit(*args, wait, self._ready_ev[slot], C.byref(t)), "ds_link_submit")
         c.content[slot] = (layer, expert)
         c.n_copies += 1
         return Transfer(slot, layer, expert, t.value)
 
     def promote(self, tr: Transfer) -> None:
         if self.cancel_enabled:
-            self.lib.call("ds_link_promote", self.handle, tr.ticket)
+            self._check(self._f_promote(self.handle, tr.ticket), "ds_link_promote")
 
     def cancel(self, tr: Transfer) -> None:
         if not self.cancel_enabled:
             return
         tr.cancelled = True
-        self.lib.call("ds_link_cancel", self.handle, tr.ticket, None)
+        self._check(self._f_cancel(self.handle, tr.ticket, None), "ds_link_cancel")
 
     def flush(self, tr: Transfer) -> None:
         """Block until every chunk of tr has been issued (its ready event recorded)."""
@@ -472,6 +488,7 @@ class Engine:
         self.max_seq, self.max_prefill = int(max_seq), int(max_prefill)
         # K4 as one device-resident graph launch per expert (A/B: DS_K4_GRAPH=0)
         self.k4_graphs = os.environ.get("DS_K4_GRAPH", "1") != "0"
+        self.front_fused = os.environ.get("DS_FRONT_FUSED", "1") != "0"
         self.kv = self._make_kv(max_seq)
         self.cos, self.sin = rope_tables(sh, max_seq, self.device)
         self.driver = None
@@ -584,7 +601,9 @@ class Engine:
         self._pa_queued = 0                   # prefetchall: layer visits queued on the copy stream
         self.hist.zero_()
         self.d2h_bytes = 0
-        self.host_wait = {"sync1": 0.0, "sync2": 0.0}     # host seconds blocked at sync points 1 / 2 (decode)
+        # host seconds blocked at sync points 1 / 2 (decode), and spent deciding
+        # after sync point 1 (gate result -> the layer's transfers submitted)
+        self.host_wait = {"sync1": 0.0, "sync2": 0.0, "decide": 0.0}
         if hasattr(self, "link"):
             self.cache.copy_stream.synchronize()
 
@@ -683,10 +702,16 @@ class Engine:
                                        self.cos, self.sin)
 
     def _decode_layer_front(self, l: int) -> None:
-        """attention(l) + rms_norm + K1 gate on static buffers (captured per layer)."""
-        h1 = self._attn_decode(l)
-        self.g_h1.copy_(h1)
-        self.g_a2.copy_(rms_norm(h1, self.W.layers[l]["ln2"], self.shape.rms_eps))
+        """attention(l) + rms_norm + K1 gate on static buffers (captured per layer).
+        Batch 1 with W4 attention: the fused front (csrc/front.cu, A/B:
+        DS_FRONT_FUSED=0); otherwise the torch ops."""
+        if self.front_fused and isinstance(self.kv, KVCache) and self.W.layers[l].get("wqkv") is not None:
+            decode_front_fused(self.shape, self.W.layers[l], self.g_h, self.kv, l, self.g_pos, self.g_mask, self.cos,
+                               self.sin, self.g_h1, self.g_a2)
+        else:
+            h1 = self._attn_decode(l)
+            self.g_h1.copy_(h1)
+            self.g_a2.copy_(rms_norm(h1, self.W.layers[l]["ln2"], self.shape.rms_eps))
         ops.gate_topk(self.g_a2, self.W.layers[l]["wg"], self.k, self.idx1, self.w1, hist=self.hist, layer=l)
 
     def _ensure_decode_graphs(self) -> None:
@@ -925,7 +950,8 @@ class Engine:
             self.driver.launch(self.hist, self.ev_gate, l + 1)     # predict stream, overlapped
         t_w = time.perf_counter()
         link.wait_event(ev_idx)                                    # sync point 1: E_l on the host
-        self.host_wait["sync1"] += time.perf_counter() - t_w
+        t_d = time.perf_counter()
+        self.host_wait["sync1"] += t_d - t_w
         self.d2h_bytes += self.idx_host.nbytes + ((4 * self.k + 8 * self.M) if use_pred else 0)
         E = [int(e) for e in self.idx_host[0].tolist()]
         if self.capture is not None:
@@ -972,6 +998,8 @@ class Engine:
             self.log.append({"phase": "decode", "token": self.t_decode, "layer": l,
                              "pred": sorted(p for p in P if p in self.owned_set),
                              "gate": sorted(E), "refetch": miss, **({"pinned": sorted(mine_pin)} if self.pinned else {})})
+        # host time from the gate result to every transfer of this layer submitted
+        self.host_wait["decide"] += time.perf_counter() - t_d
         # expert compute: pinned, then hits (already resident or in flight), then re-fetched ones
         for e in mine_pin:
             self._decode_ffn(a, self.pinned[(l, e)], E.index(e))

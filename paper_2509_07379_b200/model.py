@@ -211,6 +211,30 @@ def attention_decode_static(shape: ModelShape, L: dict, h: torch.Tensor, kv: KVC
     return _o_proj_residual(L, o, h)
 
 
+def decode_front_fused(shape: ModelShape, L: dict, h: torch.Tensor, kv: KVCache, layer: int, pos: torch.Tensor,
+                       mask: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor, h1: torch.Tensor,
+                       a2: torch.Tensor) -> None:
+    """attention_decode_static + the post-attention RMSNorm for one token, with
+    the elementwise steps in csrc/front.cu: rmsnorm -> W4 q|k|v GEMV -> RoPE +
+    KV write -> SDPA -> W4 o GEMV -> residual + rmsnorm.  Writes h1 (the
+    residual stream after attention) and a2 (the MoE block input)."""
+    nh, nkv, hd = shape.n_heads, shape.n_kv_heads, shape.head_dim
+    dev = h.device
+    a = ops.rmsnorm(h, L["ln1"], shape.rms_eps, torch.empty_like(h))
+    lin = L["wqkv"]
+    y = torch.empty((1, lin.N), dtype=torch.float32, device=dev)
+    ops.w4_linear(a, lin, y)
+    q = torch.empty((nh, hd), dtype=torch.bfloat16, device=dev)
+    ops.rope_kv_decode(y, nh, nkv, hd, cos, sin, pos, q, kv.k[layer], kv.v[layer])
+    o = F.scaled_dot_product_attention(q.view(1, nh, 1, hd), kv.k[layer].unsqueeze(0), kv.v[layer].unsqueeze(0),
+                                       attn_mask=mask, enable_gqa=True)
+    o = o.reshape(1, nh * hd)
+    lo = L["wo"]
+    yo = torch.empty((1, lo.N), dtype=torch.float32, device=dev)
+    ops.w4_linear(o, lo, yo)
+    ops.residual_rmsnorm(h, yo, L["ln2"], shape.rms_eps, h1, a2)
+
+
 def logits_last(shape: ModelShape, W: DenseWeights, h_last: torch.Tensor) -> torch.Tensor:
     return (rms_norm(h_last, W.norm, shape.rms_eps) @ W.lm_head).float()
 

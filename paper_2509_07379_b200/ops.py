@@ -152,6 +152,30 @@ def expert_gemv_graph(x: torch.Tensor, e: _lib.W4Expert, d: int, ff: int, G: int
     _count("ds_w4_down_gemv", n)
 
 
+def rmsnorm(x: torch.Tensor, gamma: torch.Tensor, eps: float, out: torch.Tensor) -> torch.Tensor:
+    R, d = x.shape
+    _lib.call("ds_rmsnorm", ptr(x), R, d, ptr(gamma), eps, ptr(out), stream_ptr())
+    _count("ds_rmsnorm")
+    return out
+
+
+def residual_rmsnorm(h: torch.Tensor, y: torch.Tensor, gamma: torch.Tensor, eps: float, h1: torch.Tensor,
+                     a: torch.Tensor) -> None:
+    R, d = h.shape
+    _lib.call("ds_residual_rmsnorm", ptr(h), ptr(y), R, d, ptr(gamma), eps, ptr(h1), ptr(a), stream_ptr())
+    _count("ds_residual_rmsnorm")
+
+
+def rope_kv_decode(y: torch.Tensor, nh: int, nkv: int, hd: int, cos: torch.Tensor, sin: torch.Tensor,
+                   pos: torch.Tensor, q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor) -> None:
+    """k_cache / v_cache: one layer's [nkv, max_seq, hd] bf16 cache; pos int64 [1] on the device."""
+    if pos.dtype != torch.int64 or not (k_cache.is_contiguous() and v_cache.is_contiguous()):
+        raise ValueError("rope_kv_decode: pos must be int64 and the caches contiguous")
+    _lib.call("ds_rope_kv_decode", ptr(y), nh, nkv, hd, ptr(cos), ptr(sin), ptr(pos), k_cache.shape[1], ptr(q),
+              ptr(k_cache), ptr(v_cache), stream_ptr())
+    _count("ds_rope_kv_decode")
+
+
 def k4_device_span() -> tuple:
     """(ns, launches): device-clock totals of every fused K4 launch so far."""
     ns, n = C.c_ulonglong(0), C.c_ulonglong(0)
