@@ -30,6 +30,11 @@ inline int cuda_status(cudaError_t e, const char* what) {
 
 int num_sms();
 
+// True the first time `key` (a kernel's address) is seen on the current
+// device: per-device one-time setup such as cudaFuncSetAttribute, which is a
+// per-device property (a process may drive several GPUs).
+bool first_use_on_device(const void* key);
+
 // ---- launch gate (measurement hygiene for CUDA-event kernel spans) -------
 // A span [ev_start, ev_end] recorded on an idle stream around host-side
 // launches also contains the host's submission latency (the start event fires

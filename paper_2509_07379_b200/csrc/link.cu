@@ -443,12 +443,9 @@ extern "C" int ds_h2d_tma_copy(void* dst, const void* src_host, size_t bytes, in
     cudaError_t e = cudaHostGetDevicePointer(&dsrc, const_cast<void*>(src_host), 0);
     if (e != cudaSuccess) return cuda_status(e, "ds_h2d_tma_copy: source is not mapped pinned host memory");
     if (bytes == 0) return DS_OK;
-    static bool attr = false;
     const int smem = ds_zc::kTmaChunk * ds_zc::kTmaSlots;
-    if (!attr) {
+    if (ds::first_use_on_device((const void*)ds_zc::tma_copy_kernel))
         cudaFuncSetAttribute(ds_zc::tma_copy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr = true;
-    }
     ds_zc::tma_copy_kernel<<<ctas, 32, smem, ds::as_stream(stream)>>>(static_cast<uint8_t*>(dst),
                                                                       static_cast<const uint8_t*>(dsrc), bytes);
     DS_LAUNCH_CHECK("ds_h2d_tma_copy");

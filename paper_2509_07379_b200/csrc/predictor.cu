@@ -475,12 +475,10 @@ int run_forward(const ds_mlp_desc* d, const double* packed, const StateArgs* s, 
         for (int i = 0; i < plan.n_layers; ++i) max_ld = plan.layer[i].ld > max_ld ? plan.layer[i].ld : max_ld;
         size_t smem = (size_t)B * max_ld * sizeof(double);
         const void* fn = B == 1 ? (const void*)mlp_fused_kernel<1> : (const void*)mlp_fused_kernel<kFusedMaxB>;
-        static bool attr_set = false;
-        if (!attr_set) {
+        if (first_use_on_device((const void*)mlp_fused_kernel<1>)) {
             cudaFuncSetAttribute(mlp_fused_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
             cudaFuncSetAttribute(mlp_fused_kernel<kFusedMaxB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  200 * 1024);
-            attr_set = true;
         }
         if (smem > 200 * 1024) return fail(DS_ERR_UNSUPPORTED, "ds_predictor: layer too wide");
         // CTAs of the persistent kernel (one per SM by default); DS_K5_CTAS caps it

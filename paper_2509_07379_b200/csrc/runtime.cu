@@ -70,6 +70,15 @@ GateState* gate_state() {
 }
 }  // namespace
 
+bool first_use_on_device(const void* key) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> seen;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    return seen.insert({key, dev}).second;
+}
+
 bool gate_warm(uint64_t key) {
     static std::mutex mu;
     static std::set<uint64_t> seen;

@@ -911,11 +911,9 @@ static int check_gemv_shape(int R, int d, int ff, int G) {
 template <int R, int G, int U, bool GUARD>
 static int swiglu_launch_u(const __nv_bfloat16* x, const ds_w4_expert* e, int d, int ff, __nv_bfloat16* h,
                            cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
+    if (first_use_on_device((const void*)swiglu_gemv_kernel<R, G, U, GUARD>)) {
         cudaFuncSetAttribute(swiglu_gemv_kernel<R, G, U, GUARD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              200 * 1024);
-        attr = true;
     }
     const size_t smem = (size_t)R * d * 2 + (size_t)R * (d / 32) * 4;
     const int grid = gemv_grid((const void*)swiglu_gemv_kernel<R, G, U, GUARD>, smem, ff);
@@ -927,12 +925,9 @@ static int swiglu_launch_u(const __nv_bfloat16* x, const ds_w4_expert* e, int d,
 template <int R, int G, int U, bool GUARD>
 static int down_launch_u(const __nv_bfloat16* h, const ds_w4_expert* e, int d, int ff, const float* rw, int rs,
                          float* acc, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
+    if (first_use_on_device((const void*)down_gemv_kernel<R, G, U, GUARD>))
         cudaFuncSetAttribute(down_gemv_kernel<R, G, U, GUARD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              200 * 1024);
-        attr = true;
-    }
     const size_t smem = (size_t)R * ff * 2 + (size_t)R * (ff / 32) * 4;
     const int grid = gemv_grid((const void*)down_gemv_kernel<R, G, U, GUARD>, smem, d);
     cudaLaunchConfig_t cfg = {};   // PDL: launch overlaps the SwiGLU GEMV's tail
@@ -1127,10 +1122,10 @@ static int staged_mma_launch(const __nv_bfloat16* x, W4Ptr a, W4Ptr b, int N, __
         int s_ = (k4s::kSmemBudget - XB - RED - 16) / (Gm::STAGE_B + 20);
         if (s_ > 8) s_ = 8;
         smem = (size_t)XB + (size_t)s_ * Gm::STAGE_B + 16 * (size_t)s_ + 4 * (size_t)((s_ + 3) & ~3) + RED;
-        if (s_ >= 2)
-            cudaFuncSetAttribute(staged_mma_swiglu_kernel<CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         S = s_;
     }
+    if (S >= 2 && first_use_on_device((const void*)staged_mma_swiglu_kernel<CPL>))
+        cudaFuncSetAttribute(staged_mma_swiglu_kernel<CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (S < 2) return 1;
     const int grid = N / 16 < num_sms() ? N / 16 : num_sms();
     static const bool want_dbg = getenv("DS_K4_TIMELINE") != nullptr;
@@ -1558,13 +1553,10 @@ static int expert_v6_launch(const __nv_bfloat16* x, const ds_w4_expert* e, __nv_
     if constexpr (S < 2 || !Gm::h_fits(S)) {
         return 1;
     } else {
-        static bool init = false;
         const size_t smem = Gm::smem(S);
-        if (!init) {
+        if (first_use_on_device((const void*)expert_fused_v6_kernel<KA, KB, RBA, RBB>))
             cudaFuncSetAttribute(expert_fused_v6_kernel<KA, KB, RBA, RBB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem);
-            init = true;
-        }
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(num_sms());
         cfg.blockDim = dim3(k4f::kThreads);
@@ -1623,11 +1615,11 @@ static int staged_launch(const __nv_bfloat16* x, W4Ptr a, W4Ptr b, int N, __nv_b
         // with mbarrier parity waits that phase would alias the awaited one
         s_ -= s_ % (k4s::kConsumers / RB);
         smem = (size_t)Gm::X_B + (size_t)s_ * Gm::STAGE_B + 20 * (size_t)s_;
-        if (s_ >= 2)
-            cudaFuncSetAttribute(staged_gemv_kernel<NMAT, CPL, G, RB, SWIGLU>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         S = s_;
     }
+    if (S >= 2 && first_use_on_device((const void*)staged_gemv_kernel<NMAT, CPL, G, RB, SWIGLU>))
+        cudaFuncSetAttribute(staged_gemv_kernel<NMAT, CPL, G, RB, SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
     if (S < 2 || S < k4s::kConsumers / RB) return 1;   // every consumer group needs its own slot
     static const int gcap = getenv("DS_K4S_GRID") ? atoi(getenv("DS_K4S_GRID")) : 0;   // A/B runs
     int grid = N < num_sms() ? N : num_sms();
@@ -1774,11 +1766,8 @@ extern "C" int ds_w4_swiglu_gemv(const void* x, int R, const ds_w4_expert* e, in
         constexpr int P = 6;
         const int NG = d / 128, S = mma_gemv_warps(NG, 2), ngw = (NG + S - 1) / S;
         const size_t smem = (size_t)S * (mma_gemv_ring_bytes<2, P>() + mma_gemv_aux_bytes(2, ngw));
-        static bool attr = false;
-        if (!attr) {
+        if (first_use_on_device((const void*)mma_gemv_kernel<2, P>))
             cudaFuncSetAttribute(mma_gemv_kernel<2, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            attr = true;
-        }
         for (int r0 = 0; r0 < R; r0 += kTok) {
             const int rr = R - r0 < kTok ? R - r0 : kTok;
             mma_gemv_kernel<2, P><<<ff / 16, 32 * S, smem, st>>>(xb + (size_t)r0 * d, rr, to_ptr(e->w1),
@@ -1809,11 +1798,8 @@ extern "C" int ds_w4_down_gemv(const void* h, int R, const ds_w4_expert* e, int 
         constexpr int P = 8;
         const int NG = ff / 128, S = mma_gemv_warps(NG, 1), ngw = (NG + S - 1) / S;
         const size_t smem = (size_t)S * (mma_gemv_ring_bytes<1, P>() + mma_gemv_aux_bytes(1, ngw));
-        static bool attr = false;
-        if (!attr) {
+        if (first_use_on_device((const void*)mma_gemv_kernel<1, P>))
             cudaFuncSetAttribute(mma_gemv_kernel<1, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            attr = true;
-        }
         for (int r0 = 0; r0 < R; r0 += kTok) {
             const int rr = R - r0 < kTok ? R - r0 : kTok;
             // PDL: the down GEMV's weight prologue overlaps the SwiGLU GEMV's tail

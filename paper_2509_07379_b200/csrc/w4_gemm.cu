@@ -502,12 +502,10 @@ template <int NMAT, int TN>
 int launch_gemm(const CUtensorMap& map, GemmArgs& a, int E, int max_mblocks, cudaStream_t st) {
     if (!plan_smem<NMAT, TN>(a))
         return fail(DS_ERR_ARG, "w4_gemm: k-range of %d k-tiles does not fit the shared-memory plan", a.kt_per_split);
-    static bool attr = false;
-    if (!attr) {
+    if (first_use_on_device((const void*)w4_gemm_kernel<NMAT, TN>)) {
         cudaError_t e = cudaFuncSetAttribute(w4_gemm_kernel<NMAT, TN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              227 * 1024);
         if (e != cudaSuccess) return cuda_status(e, "w4_gemm: smem attribute");
-        attr = true;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((a.N / BM) * a.splits, max_mblocks, E);

@@ -14,6 +14,7 @@ for s in $STEPS; do
     tests)  log tests;  timeout 1200 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; log "tests rc=$?";;
     smoke)  log smoke;  timeout 300 python -c 'import __graft_entry__ as g; g.smoke()' > gpurun_out/smoke.log 2>&1; log "smoke rc=$?";;
     bench)  log bench;  timeout 1500 python bench.py --steps 2 --warmup 3 --out gpurun_out/bench.json > gpurun_out/bench.log 2>&1; log "bench rc=$?";;
+    benchfull) log benchfull; timeout 1800 python bench.py --gpus 1 --steps 20 --warmup 5 --out gpurun_out/bench_full.json > gpurun_out/bench_full.log 2>&1; log "benchfull rc=$?";;
     bench22) log bench22; timeout 2400 python bench.py --config mixtral-8x22b --steps 1 --warmup 3 --warmup-decode 8 --no-cpu-baseline --out gpurun_out/bench22.json > gpurun_out/bench22.log 2>&1; log "bench22 rc=$?";;
     benchref) log benchref; timeout 600 python bench.py --impl reference --steps 1 --warmup 1 > gpurun_out/bench_ref.log 2>&1; log "benchref rc=$?";;
     sweep)  log sweep;  timeout 2400 python bench.py --sweep --sweep-decode 8 --out gpurun_out/sweep.json > gpurun_out/sweep.log 2>&1; log "sweep rc=$?";;
