@@ -32,9 +32,14 @@ for s in $STEPS; do
       log launches
       DS_LAUNCH_GATE=0 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "timed/" \
         --csv --log-file gpurun_out/launches.csv \
-        python bench.py --steps 1 --warmup 1 --decode 4 --warmup-decode 2 --no-cpu-baseline > gpurun_out/launches.log 2>&1
+        python bench.py --steps 1 --warmup 1 --decode 4 --warmup-decode 2 --no-cpu-baseline --no-parity --also-22b 0 > gpurun_out/launches.log 2>&1
       log "launches rc=$?"
       python scripts/summarize_launches.py gpurun_out/launches.csv > gpurun_out/launches_summary.md 2>&1;;
+    ncuv6)
+      log ncuv6
+      DS_LAUNCH_GATE=0 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'expert_fused_v6' -s 2 -c 2 \
+        -o gpurun_out/k4v6 -f python scripts/kbench.py --only k4 --iters 3 > gpurun_out/ncu_k4v6.log 2>&1
+      log "ncu k4v6 rc=$?";;
     ncu)
       log ncu
       DS_LAUNCH_GATE=0 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'expert_fused_v6|staged_gemv|swiglu_gemv|down_gemv' -s 4 -c 4 \
