@@ -32,7 +32,7 @@ for s in $STEPS; do
       log launches
       DS_LAUNCH_GATE=0 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "timed/" \
         --csv --log-file gpurun_out/launches.csv \
-        python bench.py --steps 1 --warmup 1 --decode 4 --warmup-decode 2 --no-cpu-baseline --no-parity --also-22b 0 > gpurun_out/launches.log 2>&1
+        python bench.py --steps 1 --warmup 1 --decode 4 --warmup-decode 2 --no-cpu-baseline --no-parity --also-22b 0 --calib-requests 1 --calib-decode 4 > gpurun_out/launches.log 2>&1
       log "launches rc=$?"
       python scripts/summarize_launches.py gpurun_out/launches.csv > gpurun_out/launches_summary.md 2>&1;;
     ncuv6)
