@@ -197,6 +197,9 @@ int ds_w4_graph_cache_clear(void);
  * of first-CTA-entry -> last-CTA-exit in ns and the launch count (synchronous
  * read; the profiler's in-loop kernel duration beside its CUDA-event spans). */
 int ds_k4_device_span(unsigned long long *ns, unsigned long long *n);
+/* The same for K3: every grouped FFN call given span events (GEMM1's first
+ * CTA entry -> a one-thread kernel queued right after the call's last one). */
+int ds_k3_device_span(unsigned long long *ns, unsigned long long *n);
 /* ------------------------------------------------------------------------
  * Decode front of one token (the non-MoE steps between two MoE layers; no
  * reference counterpart — the reference has no forward pass — but they sit

@@ -86,6 +86,7 @@ _SIGS = {
     "ds_residual_rmsnorm": (_I, [_P, _P, _I, _I, _P, C.c_float, _P, _P, _P]),
     "ds_rope_kv_decode": (_I, [_P, _I, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P]),
     "ds_k4_device_span": (_I, [C.POINTER(C.c_ulonglong), C.POINTER(C.c_ulonglong)]),
+    "ds_k3_device_span": (_I, [C.POINTER(C.c_ulonglong), C.POINTER(C.c_ulonglong)]),
     "ds_combine_finalize": (_I, [_P, _P, _I, _I, _P, _P]),
     "ds_w4_grouped_ffn_workspace": (_SZ, [_I, _I, _I]),
     "ds_w4_linear_layout": (_SZ, [_I, _I, _I, C.POINTER(_SZ * 3)]),

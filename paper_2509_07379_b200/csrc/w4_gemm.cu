@@ -58,6 +58,7 @@ struct GemmArgs {
     int K, N, G;
     int kt_per_split;   // k-tiles (of BK) per split
     int diag;           // diagnostics only (DS_K3_DIAG): 1 = no MMAs, 2 = no dequant, 3 = no activation
+    int span;           // GEMM1: record the device-clock span start (a timed call)
                         // loads, 4 = no code loads (results invalid)
     int n_eff;          // UMMA N actually issued (multiple of 16, <= TN): the token rows of a single
                         // m-block rounded up to 16, so a 151-row expert costs N = 160, not 256
@@ -180,6 +181,20 @@ __device__ __forceinline__ void dequant32(const uint4 c, uint32_t zz, uint32_t s
 // stamps [NMAT - 1][cta][8]: 0 entry, 1 scales staged, 2 first MMA issued,
 // 3 last MMA issued, 4 accumulators ready, 5 exit
 __device__ unsigned long long g_k3_dbg[2][1024][8];
+// device-clock span of a timed grouped FFN call (its CUDA events also carry
+// the event-timestamp cost under host-link load, profiles/r2/graph_k4): every
+// GEMM1 CTA records ~entry time (zero-initialised atomicMax finds the
+// earliest); a one-thread kernel queued after the call's last kernel closes
+// the span (+ one launch gap) and accumulates it.
+__device__ unsigned long long g_k3_first, g_k3_span_ns, g_k3_span_n;
+
+__global__ void k3_span_close_kernel() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const unsigned long long first = ~atomicExch(&g_k3_first, 0ull);
+    atomicAdd(&g_k3_span_ns, t - first);
+    atomicAdd(&g_k3_span_n, 1ull);
+}
 __device__ __forceinline__ void k3_stamp(int diag, int nmat, int slot) {
     if (diag != 8) return;
     const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
@@ -211,6 +226,11 @@ w4_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constan
     uint64_t* s_full = tmem_full + 1;                 // the n-block's scales / zeros staged
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 1);
 
+    if (NMAT == 2 && args.span && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        atomicMax(&g_k3_first, ~t);
+    }
     const int e = blockIdx.z;
     const int rows = args.rows[e];
     const int m0 = blockIdx.y * TN;
@@ -627,6 +647,7 @@ static int grouped_ffn_impl(const void* xperm, const int32_t* row_start, const i
     GemmArgs a1{}, a2{};
     static const int diag = getenv("DS_K3_TIMELINE") ? 8 : (getenv("DS_K3_DIAG") ? atoi(getenv("DS_K3_DIAG")) : 0);
     a1.diag = a2.diag = diag;
+    a1.span = ev_start != nullptr;
     // token tile: 256 rows (UMMA N = 256) once an expert has more than 128 rows,
     // so its weights are dequantised once instead of once per 128-row block
     int max_rows = 0;
@@ -709,12 +730,26 @@ static int grouped_ffn_impl(const void* xperm, const int32_t* row_start, const i
             if (er != cudaSuccess) rc = cuda_status(er, "ds_w4_grouped_ffn: split reduce");
         }
     }
+    if (!rc && ev_start) {
+        k3_span_close_kernel<<<1, 1, 0, st>>>();
+        cudaError_t er = cudaGetLastError();
+        if (er != cudaSuccess) rc = cuda_status(er, "ds_w4_grouped_ffn: span");
+    }
     if (!rc && ev_end) {
         cudaError_t er = cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_end), st);
         if (er != cudaSuccess) rc = cuda_status(er, "ds_w4_grouped_ffn: event");
     }
     gate_release(gate);                 // on every path: a held stream must never stay blocked
     return rc;
+}
+
+// Device-clock totals of every timed grouped FFN call (GEMM1's first CTA entry
+// -> a one-thread kernel right after the call's last kernel).
+extern "C" int ds_k3_device_span(unsigned long long* ns, unsigned long long* n) {
+    DS_CHECK_ARG(ns && n, "ds_k3_device_span: NULL pointer");
+    cudaError_t e = cudaMemcpyFromSymbol(ns, g_k3_span_ns, sizeof(*ns));
+    if (e == cudaSuccess) e = cudaMemcpyFromSymbol(n, g_k3_span_n, sizeof(*n));
+    return cuda_status(e, "ds_k3_device_span");
 }
 
 // Plain W4 linear for many rows (prefill attention projections): y[rows, N]

@@ -183,6 +183,13 @@ def k4_device_span() -> tuple:
     return ns.value, n.value
 
 
+def k3_device_span() -> tuple:
+    """(ns, calls): device-clock totals of every timed grouped-FFN (K3) call so far."""
+    ns, n = C.c_ulonglong(0), C.c_ulonglong(0)
+    _lib.call("ds_k3_device_span", C.byref(ns), C.byref(n))
+    return ns.value, n.value
+
+
 def w4_graph_cache_clear() -> None:
     _lib.call("ds_w4_graph_cache_clear")
 
