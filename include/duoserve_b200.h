@@ -13,7 +13,9 @@
  *   - plain pointers and sizes only; device pointers are caller-owned
  *     (allocated by the caller, e.g. as torch tensors), "stream" is a
  *     cudaStream_t passed as void*; no entry point allocates device memory
- *     (the diagnostic DS_K4_TIMELINE switch excepted);
+ *     (the diagnostic DS_K4_TIMELINE switch excepted; the driver-managed
+ *     executables of ds_w4_expert_gemv_graph's graph cache are released by
+ *     ds_w4_graph_cache_clear);
  *   - return 0 on success, a positive cudaError_t on a CUDA failure, or a
  *     negative DS_ERR_* on invalid arguments; ds_last_error() returns the
  *     calling thread's last message;
