@@ -60,9 +60,15 @@ struct ds_link {
     std::vector<cudaEvent_t> pool;
     uint64_t next_ticket = 1;
     uint64_t bytes_issued = 0, bytes_wasted = 0, chunks = 0;
-    // trace mode: a timing event pair around every chunk (copy-busy intervals
-    // for the copy/compute overlap fraction); off by default
+    // trace mode: a timing event pair around every transfer's run of chunks
+    // (copy-busy intervals for the copy/compute overlap fraction); off by
+    // default.  One pair per transfer, not per chunk: while the copy engine
+    // streams host memory a timing event costs ~22 us of stream time
+    // (profiles/r2/graph_k4), so per-chunk events would stall the very link
+    // they measure.  The open span of the transfer being issued:
     bool trace = false;
+    const void* trace_x = nullptr;
+    cudaEvent_t trace_t0 = nullptr;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> spans;
     std::vector<cudaEvent_t> tpool;
     int error = 0;
@@ -95,6 +101,16 @@ cudaEvent_t take_timing_event(ds_link* L) {
     return e;
 }
 
+// Close the open trace span after the chunks issued so far.  L->mu held.
+void trace_close_locked(ds_link* L) {
+    if (!L->trace_x) return;
+    cudaEvent_t t1 = take_timing_event(L);
+    cudaEventRecord(t1, L->stream);
+    L->spans.emplace_back(L->trace_t0, t1);
+    L->trace_x = nullptr;
+    L->trace_t0 = nullptr;
+}
+
 // Issue as many chunks as the depth allows.  Called with L->mu held.
 void issue_locked(ds_link* L) {
     while (!L->inflight.empty() && cudaEventQuery(L->inflight.front()) == cudaSuccess) {
@@ -105,18 +121,14 @@ void issue_locked(ds_link* L) {
         auto x = L->pending.front();
         if (x->next == 0 && x->wait_ev) cudaStreamWaitEvent(L->stream, x->wait_ev, 0);
         const size_t n = std::min(x->chunk ? x->chunk : L->chunk, x->bytes - x->next);
-        cudaEvent_t t0 = nullptr, t1 = nullptr;
-        if (L->trace) {
-            t0 = take_timing_event(L);
-            t1 = take_timing_event(L);
-            cudaEventRecord(t0, L->stream);
+        if (L->trace && L->trace_x != x.get()) {
+            trace_close_locked(L);                    // the previous transfer (e.g. a cancelled one) ends here
+            L->trace_t0 = take_timing_event(L);
+            cudaEventRecord(L->trace_t0, L->stream);
+            L->trace_x = x.get();
         }
         cudaError_t e = cudaMemcpyAsync(x->dst + x->next, x->src + x->next, n, cudaMemcpyHostToDevice, L->stream);
         if (e != cudaSuccess) L->error = (int)e;
-        if (L->trace) {
-            cudaEventRecord(t1, L->stream);
-            L->spans.emplace_back(t0, t1);
-        }
         cudaEvent_t ev = take_event(L);
         cudaEventRecord(ev, L->stream);
         L->inflight.push_back(ev);
@@ -124,6 +136,7 @@ void issue_locked(ds_link* L) {
         L->bytes_issued += n;
         L->chunks++;
         if (x->next >= x->bytes) {
+            if (L->trace) trace_close_locked(L);
             if (x->done_ev) cudaEventRecord(x->done_ev, L->stream);
             x->issued = true;
             L->pending.pop_front();
@@ -185,6 +198,7 @@ extern "C" int ds_link_destroy(ds_link* L) {
         cudaEventDestroy(sp.second);
     }
     for (auto e : L->tpool) cudaEventDestroy(e);
+    if (L->trace_t0) cudaEventDestroy(L->trace_t0);
     delete L;
     return DS_OK;
 }
@@ -251,6 +265,9 @@ extern "C" int ds_link_cancel(ds_link* L, uint64_t ticket, size_t* bytes_issued)
         auto x = it->second;
         done = x->next;
         x->cancelled = true;
+        // its trace span ends after the chunks already in flight (recorded now,
+        // not when the next transfer starts: the link may idle in between)
+        if (L->trace && L->trace_x == x.get()) trace_close_locked(L);
         L->bytes_wasted += x->next;
         for (auto p = L->pending.begin(); p != L->pending.end(); ++p)
             if ((*p)->ticket == ticket) {
@@ -298,6 +315,7 @@ extern "C" int ds_link_reset_stats(ds_link* L) {
 extern "C" int ds_link_trace(ds_link* L, int enable) {
     DS_CHECK_ARG(L, "ds_link_trace: NULL link");
     std::lock_guard<std::mutex> g(L->mu);
+    if (!enable) trace_close_locked(L);
     L->trace = enable != 0;
     return DS_OK;
 }
@@ -310,6 +328,7 @@ extern "C" int ds_link_trace_read(ds_link* L, void* ref_event, float* start_ms, 
                                   size_t* n_out) {
     DS_CHECK_ARG(L && ref_event && n_out, "ds_link_trace_read: bad arguments");
     std::lock_guard<std::mutex> g(L->mu);
+    trace_close_locked(L);                            // a transfer cut short by a cancellation
     cudaEvent_t ref = static_cast<cudaEvent_t>(ref_event);
     size_t n = 0;
     int err = 0;
