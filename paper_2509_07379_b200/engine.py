@@ -513,6 +513,7 @@ class Engine:
         self.idx1 = torch.empty((B, self.k), dtype=torch.int32, device=dev)
         self.w1 = torch.empty((B, self.k), dtype=torch.float32, device=dev)
         self.idx_host = torch.empty((B, self.k), dtype=torch.int32, pin_memory=True)
+        self._idx_np = self.idx_host.numpy()        # same memory: read at sync point 1 without torch indexing
         self.h_buf = torch.empty((1, self.ff), dtype=torch.bfloat16, device=dev)
         self.acc = torch.zeros((1, self.d), dtype=torch.float32, device=dev)
         self.ev_gate = torch.cuda.Event()
@@ -953,7 +954,7 @@ class Engine:
         t_d = time.perf_counter()
         self.host_wait["sync1"] += t_d - t_w
         self.d2h_bytes += self.idx_host.nbytes + ((4 * self.k + 8 * self.M) if use_pred else 0)
-        E = [int(e) for e in self.idx_host[0].tolist()]
+        E = self._idx_np[0].tolist()
         if self.capture is not None:
             self.capture.append(("decode", l, a.cpu(), self.idx_host.clone()))
         slot_of, trs = {}, {}
@@ -982,12 +983,13 @@ class Engine:
             P, order, pending = self._pred_next              # pending: this rank's predicted experts
             miss = sorted(set(mine) - set(P))
             spare = [pending[p][0] for p in order if p in pending and p not in E]
+            confirmed = []
             for p in order:
                 if p not in pending:
                     continue
                 if p in E:
                     slot_of[p], trs[p] = pending[p]
-                    link.promote(trs[p])                       # confirmed: finish with large chunks
+                    confirmed.append(trs[p])
                 else:
                     link.cancel(pending[p][1])                 # drop its not-yet-issued chunks
             used = set(slot_of.values())
@@ -995,6 +997,8 @@ class Engine:
             for e, s_ in zip(miss, spare):
                 trs[e] = link.submit(s_, l, e)                 # re-fetch into a wrong (or free) slot
                 slot_of[e] = s_
+            for tr in confirmed:                               # after the re-fetches: they wait on no promote
+                link.promote(tr)                               # confirmed: finish with large chunks
             self.log.append({"phase": "decode", "token": self.t_decode, "layer": l,
                              "pred": sorted(p for p in P if p in self.owned_set),
                              "gate": sorted(E), "refetch": miss, **({"pinned": sorted(mine_pin)} if self.pinned else {})})
